@@ -1,0 +1,142 @@
+/*
+ * exactz.h — C ABI of the B200 (sm_100a) EXaCTz topology-correction hot path.
+ *
+ * The operation (PAPER.md, arXiv 2604.01397):
+ *   Alg. 1: given the original field f, its decompressed version
+ *   f^ with |f_i - f^_i| <= xi and the bound xi, set g <- f^ and repeat
+ *     S <- CheckConstraints(g, f)        (C1 P:284-290, C2 P:292-294,
+ *                                         C3 P:297-302)
+ *     if S is empty: stop
+ *     g <- ApplyBoundedEdits(g, S, xi)   (one step Delta = xi/N down,
+ *                                         lossless clamp f - xi after N steps)
+ *   The returned field g (and the per-vertex edit counts = the edit set E)
+ *   preserve the extremum graph and the join/split trees of f.
+ *
+ * Exact semantics (bit-level) are SURVEY.md §8(c) O0-O10 with the readings
+ * listed in DESIGN.md §3; the CPU oracle (oracle/) implements the same
+ * definition independently and the test suite checks bit equality.
+ *
+ * Conventions common to every call
+ *  - Grid: dims = {nx, ny, nz}; nz = 1 gives the 2D path, ny = nz = 1 a 1D
+ *    path.  Linear index i = x + nx*(y + ny*z) (x fastest); V = nx*ny*nz must
+ *    be < 2^31 (labels are int32 global ids).
+ *  - Mesh: Freudenthal/Kuhn triangulation (14 neighbours, clipped at faces).
+ *  - Order: Simulation of Simplicity (P:178 footnote): u < v iff
+ *    h_u < h_v or (h_u == h_v and u < v), IEEE compares (-0 == +0).
+ *  - Values: float32; every f and f^ value must be finite.
+ *  - Ownership: the caller owns every buffer.  Scratch is allocated with
+ *    cudaMallocAsync on `stream` and freed before return.  f and g_in are
+ *    never written unless out == g_in (allowed).
+ *  - Device pointers: unless a name ends in _host, array arguments are CUDA
+ *    device pointers of the current device, 16-byte aligned.  `stream` is a
+ *    cudaStream_t (NULL = legacy default stream).
+ *  - Blocking: every call returns after the result is known on the host
+ *    (*iters etc.); device outputs are complete in stream order.
+ *  - Errors: no exception crosses the ABI.  Validation failures (EXACTZ_EINVAL,
+ *    EXACTZ_EBOUND) return before anything is written to `out`.  CUDA errors
+ *    map to EXACTZ_ECUDA, allocation failures to EXACTZ_ENOMEM; details in
+ *    exactz_last_error() (thread-local).
+ */
+#ifndef EXACTZ_H
+#define EXACTZ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  EXACTZ_OK = 0,
+  EXACTZ_EINVAL = 2,       /* null pointer, bad dims, non-finite value, N out of range */
+  EXACTZ_EBOUND = 3,       /* some f^_i outside [RU(f_i - xi), RD(f_i + xi)] */
+  EXACTZ_ESTUCK = 4,       /* violations remain at a fixpoint or at max_iters (amb-17) */
+  EXACTZ_EUNSUPPORTED = 5, /* requested mode not built */
+  EXACTZ_ECUDA = 6,
+  EXACTZ_ENCCL = 7,
+  EXACTZ_ENOMEM = 8
+} exactz_status;
+
+/* debug flags */
+#define EXACTZ_NO_C2 0x1u /* skip the saddle-ordering rule (C2, R4) */
+#define EXACTZ_NO_C3 0x2u /* skip the event rules (C3, R5/R6) */
+
+/* One row per CheckConstraints pass (the last row is the clean pass on OK). */
+typedef struct {
+  uint64_t violations; /* V_t: distinct vertices marked for an edit */
+  uint64_t applied;    /* edits applied this round (marked and not yet at f - xi) */
+  uint64_t n[6];       /* per-rule counts: R1 max-neighbour, R2 min-neighbour,
+                          R3 flipped (vertex, link-vertex) pairs at saddles / type
+                          changes, R4 flipped adjacent saddles, R5 join events,
+                          R6 split events */
+} exactz_iter_stats;
+
+typedef struct {
+  exactz_iter_stats *rows; /* HOST array of `cap` rows, may be NULL */
+  uint32_t cap;
+  uint32_t nrows;          /* out: number of detection passes (may exceed cap) */
+  double ms_setup;         /* out: validate + reference setup (CUDA events) */
+  double ms_loop;          /* out: all iterations */
+} exactz_stats;
+
+typedef struct {
+  uint32_t N;            /* steps before the lossless clamp; 0 => 5; <= 254 */
+  uint32_t max_iters;    /* 0 => none: the loop ends at a fixpoint */
+  uint32_t flags;        /* EXACTZ_NO_C2 | EXACTZ_NO_C3 */
+  uint8_t *edit_counts;  /* optional out [V]: c_i in 0..N+1, N+1 == stored losslessly */
+  int32_t *label_min;    /* optional out [V]: steepest-descent terminus of i in out */
+  int32_t *label_max;    /* optional out [V]: steepest-ascent terminus of i in out */
+  exactz_stats *stats;   /* optional HOST struct */
+} exactz_opts;
+
+/* The iterative correction (Alg. 1).  Returns EXACTZ_OK with zero violations
+ * left, or EXACTZ_ESTUCK with out = the last g.  *iters (HOST) = number of
+ * edit rounds (0 when f^ is already clean). */
+exactz_status exactz_correct(const float *f, const float *g_in, const int64_t dims[3],
+                             float eps_abs, float *out, uint32_t *iters,
+                             const exactz_opts *opts, void *stream);
+
+/* Same call with HOST buffers (f_host, g_in_host, out_host and the optional
+ * opts arrays are host memory; pinned memory is fastest).  The host<->device
+ * copies are part of the call. */
+exactz_status exactz_correct_host(const float *f_host, const float *g_in_host,
+                                  const int64_t dims[3], float eps_abs, float *out_host,
+                                  uint32_t *iters, const exactz_opts *opts_host, void *stream);
+
+/* One CheckConstraints(g, f) pass without editing: *violations (HOST)
+ * = V_t, per-rule counts into row (HOST, may be NULL).  g must satisfy the
+ * bound (else EXACTZ_EBOUND).  Used to verify a corrected field. */
+exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3], float eps_abs,
+                           uint64_t *violations, exactz_iter_stats *row, uint32_t flags,
+                           void *stream);
+
+/* xi = RN_f32(rel * (max f - min f)) computed in double (amb-19). */
+exactz_status exactz_eps_from_relative(const float *f, int64_t n, double rel, float *eps_abs,
+                                       void *stream);
+
+/* Sharded variant: z-slabs, one rank per GPU, NCCL over NVLink.  Collective:
+ * every rank calls with identical scalars.  `id` is 128 bytes from
+ * exactz_nccl_unique_id on rank 0, broadcast by the caller. */
+typedef struct exactz_comm exactz_comm;
+exactz_status exactz_nccl_unique_id(uint8_t id[128]);
+exactz_status exactz_comm_init(const uint8_t id[128], int nranks, int rank, int cuda_device,
+                               exactz_comm **out);
+exactz_status exactz_comm_destroy(exactz_comm *comm);
+/* f_local / g_local / out_local: the z_count planes [z_begin, z_begin+z_count)
+ * of the global field (global_dims = {nx, ny, nz}).  out_local is bit-equal to
+ * the same planes of the single-GPU out; *iters identical on every rank. */
+exactz_status exactz_correct_sharded(exactz_comm *comm, const float *f_local,
+                                     const float *g_local, const int64_t global_dims[3],
+                                     int64_t z_begin, int64_t z_count, float eps_abs,
+                                     float *out_local, uint32_t *iters, const exactz_opts *opts,
+                                     void *stream);
+
+const char *exactz_strerror(exactz_status s);
+const char *exactz_last_error(void);
+/* build identification, e.g. "exactz sm_100a <git-describe>" */
+const char *exactz_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXACTZ_H */

@@ -1,0 +1,203 @@
+"""paper_2604_01397_b200 — B200 (sm_100a) EXaCTz topology-correction hot path.
+
+Thin Python binding of the C ABI in include/exactz.h (libexactz.so, built
+in-tree by _build.py).  Argument marshalling only: every step of the path runs
+in the CUDA kernels of csrc/.  PyTorch is used for device memory and streams.
+There is no CPU fallback: importing this package without the built library
+raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libexactz.so")
+
+OK, EINVAL, EBOUND, ESTUCK, EUNSUPPORTED, ECUDA, ENCCL, ENOMEM = 0, 2, 3, 4, 5, 6, 7, 8
+NO_C2, NO_C3 = 0x1, 0x2
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g;"
+                      " g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+
+
+class IterStats(C.Structure):
+    _fields_ = [("violations", C.c_uint64), ("applied", C.c_uint64), ("n", C.c_uint64 * 6)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("rows", C.POINTER(IterStats)), ("cap", C.c_uint32), ("nrows", C.c_uint32),
+                ("ms_setup", C.c_double), ("ms_loop", C.c_double)]
+
+
+class Opts(C.Structure):
+    _fields_ = [("N", C.c_uint32), ("max_iters", C.c_uint32), ("flags", C.c_uint32),
+                ("edit_counts", C.c_void_p), ("label_min", C.c_void_p),
+                ("label_max", C.c_void_p), ("stats", C.POINTER(Stats))]
+
+
+_lib = C.CDLL(LIB_PATH)
+_P, _i64p = C.c_void_p, C.POINTER(C.c_int64)
+_lib.exactz_correct.argtypes = [_P, _P, _i64p, C.c_float, _P, C.POINTER(C.c_uint32),
+                                C.POINTER(Opts), _P]
+_lib.exactz_correct.restype = C.c_int
+_lib.exactz_correct_host.argtypes = _lib.exactz_correct.argtypes
+_lib.exactz_correct_host.restype = C.c_int
+_lib.exactz_check.argtypes = [_P, _P, _i64p, C.c_float, C.POINTER(C.c_uint64),
+                              C.POINTER(IterStats), C.c_uint32, _P]
+_lib.exactz_check.restype = C.c_int
+_lib.exactz_eps_from_relative.argtypes = [_P, C.c_int64, C.c_double, C.POINTER(C.c_float), _P]
+_lib.exactz_eps_from_relative.restype = C.c_int
+_lib.exactz_strerror.argtypes = [C.c_int]
+_lib.exactz_strerror.restype = C.c_char_p
+_lib.exactz_last_error.restype = C.c_char_p
+_lib.exactz_version.restype = C.c_char_p
+_lib.exactz_nccl_unique_id.argtypes = [_P]
+_lib.exactz_nccl_unique_id.restype = C.c_int
+_lib.exactz_comm_init.argtypes = [_P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+_lib.exactz_comm_init.restype = C.c_int
+_lib.exactz_comm_destroy.argtypes = [_P]
+_lib.exactz_comm_destroy.restype = C.c_int
+_lib.exactz_correct_sharded.argtypes = [_P, _P, _P, _i64p, C.c_int64, C.c_int64, C.c_float, _P,
+                                        C.POINTER(C.c_uint32), C.POINTER(Opts), _P]
+_lib.exactz_correct_sharded.restype = C.c_int
+
+
+def lib() -> C.CDLL:
+    return _lib
+
+
+def version() -> str:
+    return _lib.exactz_version().decode()
+
+
+def last_error() -> str:
+    return _lib.exactz_last_error().decode()
+
+
+class ExactzError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {_lib.exactz_strerror(status).decode()} ({last_error()})")
+
+
+@dataclass
+class CorrectResult:
+    status: int            # OK or ESTUCK
+    iters: int             # edit rounds
+    stats: list            # per detection pass: (V_t, applied, n1..n6)
+    ms_setup: float
+    ms_loop: float
+
+
+def _dims(t) -> C.Array:
+    shp = list(t.shape)
+    d = list(reversed(shp)) + [1] * (3 - len(shp))
+    return (C.c_int64 * 3)(*[int(x) for x in d])
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _opts(N, max_iters, flags, edit_counts, label_min, label_max, stats_cap):
+    o = Opts()
+    o.N, o.max_iters, o.flags = N, max_iters, flags
+    o.edit_counts = None if edit_counts is None else edit_counts.data_ptr()
+    o.label_min = None if label_min is None else label_min.data_ptr()
+    o.label_max = None if label_max is None else label_max.data_ptr()
+    st = Stats()
+    rows = (IterStats * max(stats_cap, 1))()
+    st.rows = C.cast(rows, C.POINTER(IterStats)) if stats_cap else None
+    st.cap = stats_cap
+    o.stats = C.pointer(st)
+    return o, st, rows
+
+
+def _result(status, iters, st, rows):
+    n = min(st.nrows, st.cap)
+    table = [(r.violations, r.applied, *list(r.n)) for r in rows[:n]] if st.cap else []
+    return CorrectResult(status, iters.value, table, st.ms_setup, st.ms_loop)
+
+
+def exactz_correct(f, g_in, eps: float, out=None, *, N: int = 5, max_iters: int = 0,
+                   flags: int = 0, edit_counts=None, label_min=None, label_max=None,
+                   stats_cap: int = 0, stream=None) -> CorrectResult:
+    """Alg. 1 on device tensors (float32, contiguous, shape (nz,ny,nx)/(ny,nx)/(nx,)).
+
+    `out` (default: a new tensor) receives the corrected field; it may alias
+    g_in.  edit_counts (uint8), label_min/label_max (int32) are optional
+    device outputs.  Raises ExactzError unless the status is OK or ESTUCK."""
+    import torch
+    for t in (f, g_in):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValueError("f and g_in must be contiguous float32 CUDA tensors")
+    if out is None:
+        out = torch.empty_like(g_in)
+    o, st, rows = _opts(N, max_iters, flags, edit_counts, label_min, label_max, stats_cap)
+    iters = C.c_uint32(0)
+    s = _lib.exactz_correct(_ptr(f), _ptr(g_in), _dims(f), float(eps), _ptr(out), C.byref(iters),
+                            C.byref(o), _stream(stream))
+    if s not in (OK, ESTUCK):
+        raise ExactzError(s, "exactz_correct")
+    res = _result(s, iters, st, rows)
+    res.out = out
+    return res
+
+
+def exactz_correct_host(f, g_in, eps: float, out=None, *, N: int = 5, max_iters: int = 0,
+                        flags: int = 0, edit_counts=None, label_min=None, label_max=None,
+                        stats_cap: int = 0, stream=None) -> CorrectResult:
+    """Alg. 1 on HOST tensors (CPU, float32, contiguous; pinned is fastest):
+    the host<->device copies happen inside the C call."""
+    import torch
+    for t in (f, g_in):
+        if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+            raise ValueError("f and g_in must be contiguous float32 CPU tensors")
+    if out is None:
+        out = torch.empty_like(g_in)
+    o, st, rows = _opts(N, max_iters, flags, edit_counts, label_min, label_max, stats_cap)
+    iters = C.c_uint32(0)
+    s = _lib.exactz_correct_host(_ptr(f), _ptr(g_in), _dims(f), float(eps), _ptr(out),
+                                 C.byref(iters), C.byref(o), _stream(stream))
+    if s not in (OK, ESTUCK):
+        raise ExactzError(s, "exactz_correct_host")
+    res = _result(s, iters, st, rows)
+    res.out = out
+    return res
+
+
+def exactz_check(f, g, eps: float, flags: int = 0, stream=None):
+    """One CheckConstraints pass: (V_t, (n1..n6))."""
+    v = C.c_uint64(0)
+    row = IterStats()
+    s = _lib.exactz_check(_ptr(f), _ptr(g), _dims(f), float(eps), C.byref(v), C.byref(row),
+                          flags, _stream(stream))
+    if s != OK:
+        raise ExactzError(s, "exactz_check")
+    return v.value, tuple(row.n)
+
+
+def exactz_eps_from_relative(f, rel: float, stream=None) -> float:
+    e = C.c_float(0)
+    s = _lib.exactz_eps_from_relative(_ptr(f), f.numel(), float(rel), C.byref(e), _stream(stream))
+    if s != OK:
+        raise ExactzError(s, "exactz_eps_from_relative")
+    return e.value
+
+
+def status_of(fn, *a, **kw) -> int:
+    """Call fn and return its status code instead of raising (tests)."""
+    try:
+        r = fn(*a, **kw)
+        return r.status if isinstance(r, CorrectResult) else OK
+    except ExactzError as e:
+        return e.status

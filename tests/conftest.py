@@ -1,0 +1,36 @@
+"""pytest configuration: the `gpu` marker and shared fixtures.
+
+`-m "not gpu"` runs the oracle pins, host logic and the ABI/export checks (no
+GPU needed); `-m gpu` runs the parity tests that call the CUDA path through
+the C ABI."""
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libexactz.so")
+    config.addinivalue_line("markers", "slow: long-running (full-size) case")
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle import oracle as O
+    O.build()
+    return O
+
+
+@pytest.fixture(scope="session")
+def exactz():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test collected without a CUDA device")
+    from paper_2604_01397_b200 import _build
+    _build.build()
+    import paper_2604_01397_b200 as E
+    return E

@@ -1,0 +1,171 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bar (BASELINE.json north_star): bit-exact equality of the
+corrected field, the edit counts, both label arrays, the iteration count, the
+status and every per-pass counter (V_t, applied, n1..n6) on the same seeded
+inputs.  Sizes are ones the oracle finishes in seconds, shaped to span several
+x-blocks (128 wide) and rows with ragged tails.
+"""
+import numpy as np
+import pytest
+import torch
+
+from synth import fields as S
+
+pytestmark = pytest.mark.gpu
+
+
+def run_both(E, O, f, g, xi, N=5, flags=0, max_iters=0, mode_alias=False):
+    fn, gn = f.numpy(), g.numpy()
+    ro = O.correct(fn, gn, xi, N, flags=flags, max_iters=max_iters)
+    fd, gd = f.cuda(), g.cuda()
+    V = f.numel()
+    c = torch.empty(V, dtype=torch.uint8, device="cuda")
+    lmin = torch.empty(V, dtype=torch.int32, device="cuda")
+    lmax = torch.empty(V, dtype=torch.int32, device="cuda")
+    out = gd if mode_alias else None
+    rg = E.exactz_correct(fd, gd, xi, out=out, N=N, flags=flags, max_iters=max_iters,
+                          edit_counts=c, label_min=lmin, label_max=lmax, stats_cap=100000)
+    torch.cuda.synchronize()
+    return ro, rg, c.cpu().numpy(), lmin.cpu().numpy(), lmax.cpu().numpy()
+
+
+def assert_parity(ro, rg, c, lmin, lmax):
+    assert rg.status == ro.status
+    assert rg.iters == ro.iters
+    og = rg.out.reshape(-1).cpu().numpy()
+    bad = np.nonzero(og.view(np.uint32) != ro.out.view(np.uint32))[0]
+    assert bad.size == 0, f"out differs at {bad[:10]} ({bad.size} vertices)"
+    assert np.array_equal(c, ro.counts), "edit counts differ"
+    assert np.array_equal(lmin, ro.label_min), "label_min differs"
+    assert np.array_equal(lmax, ro.label_max), "label_max differs"
+    st_g = np.array(rg.stats, dtype=np.int64).reshape(-1, 8)
+    assert st_g.shape == ro.stats.shape
+    assert np.array_equal(st_g, ro.stats), "per-pass counters differ"
+
+
+CASES = [
+    ("C1", None),              # 16^3 GaussMix, rel 1e-2 (the BASELINE config itself)
+    ("C2", (20, 24, 131)),     # Nyx-like recipe, 2 x-blocks, ragged
+    ("C3", (17, 21, 150)),     # combustion recipe: many saddles, plateaus at 300 K
+    ("C4", (1, 90, 300)),      # 2D climate recipe (nz = 1), 3 x-blocks
+    ("C5", (24, 18, 40)),      # cosmology recipe at rel 1e-4
+]
+
+
+@pytest.mark.parametrize("cfg,shape", CASES)
+def test_parity_configs(exactz, oracle, cfg, shape):
+    f, g, xi = S.make(cfg, shape=shape)
+    assert_parity(*run_both(exactz, oracle, f, g, xi))
+
+
+@pytest.mark.parametrize("cfg,shape", [("C1", None), ("C3", (12, 16, 140))])
+def test_parity_sz_plateaus(exactz, oracle, cfg, shape):
+    """SZ-like binned decompression: plateaus everywhere, so SoS ties decide."""
+    f, g, xi = S.make(cfg, shape=shape, mode="sz")
+    assert_parity(*run_both(exactz, oracle, f, g, xi))
+
+
+@pytest.mark.parametrize("flags", [1, 2, 3])
+def test_parity_debug_flags(exactz, oracle, flags):
+    f, g, xi = S.make("C1")
+    assert_parity(*run_both(exactz, oracle, f, g, xi, flags=flags))
+
+
+@pytest.mark.parametrize("N", [1, 2, 9])
+def test_parity_N(exactz, oracle, N):
+    f, g, xi = S.make("C2", shape=(10, 12, 33))
+    assert_parity(*run_both(exactz, oracle, f, g, xi, N=N))
+
+
+def test_parity_max_iters(exactz, oracle):
+    f, g, xi = S.make("C1")
+    ro, rg, *rest = run_both(exactz, oracle, f, g, xi, max_iters=3)
+    assert ro.status == 4 and ro.iters == 3
+    assert_parity(ro, rg, *rest)
+
+
+def test_parity_alias_out(exactz, oracle):
+    f, g, xi = S.make("C1")
+    assert_parity(*run_both(exactz, oracle, f, g, xi, mode_alias=True))
+
+
+def test_edit_strategy_1x3(exactz, oracle):
+    """fig:edit_strategy as a 1x3 field (tests/golden/)."""
+    f = torch.tensor([3.0, 1.0, 2.0])
+    g = torch.tensor([3.0, 1.9, 1.8])
+    ro, rg, c, lmin, lmax = run_both(exactz, oracle, f, g, 1.0)
+    assert_parity(ro, rg, c, lmin, lmax)
+    assert rg.out.cpu().numpy().view(np.uint32).tolist() == [0x40400000, 0x3FD99999, 0x3FE66666]
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 1, 7), (1, 5, 1), (3, 1, 1), (2, 2, 2),
+                                   (1, 3, 129), (5, 1, 4)])
+def test_parity_degenerate_shapes(exactz, oracle, shape):
+    rs = np.random.default_rng(sum(shape))
+    f = torch.from_numpy(rs.uniform(1, 2, size=shape).astype(np.float32))
+    xi = 0.05
+    g = S.decompress(f, xi, seed=7)
+    assert_parity(*run_both(exactz, oracle, f, g, xi))
+
+
+def test_clean_input_zero_iters(exactz, oracle):
+    f, _, xi = S.make("C1")
+    ro, rg, *rest = run_both(exactz, oracle, f, f.clone(), xi)
+    assert rg.iters == 0 and rg.status == 0
+    assert_parity(ro, rg, *rest)
+
+
+def test_xi_zero(exactz, oracle):
+    f, _, _ = S.make("C1")
+    ro, rg, *rest = run_both(exactz, oracle, f, f.clone(), 0.0)
+    assert rg.status == 0 and rg.iters == 0
+    assert_parity(ro, rg, *rest)
+
+
+def test_errors(exactz):
+    E = exactz
+    f, g, xi = S.make("C1")
+    fd, gd = f.cuda(), g.cuda()
+    bad = gd.clone()
+    bad.view(-1)[100] = f.view(-1)[100] + 2 * xi
+    out = torch.full_like(gd, 7.0)
+    assert E.status_of(E.exactz_correct, fd, bad, xi, out=out) == E.EBOUND
+    assert bool((out == 7.0).all()), "out written before validation failed"
+    nan = gd.clone()
+    nan.view(-1)[5] = float("nan")
+    assert E.status_of(E.exactz_correct, fd, nan, xi) == E.EINVAL
+    assert E.status_of(E.exactz_correct, fd, gd, -1.0) == E.EINVAL
+    assert E.status_of(E.exactz_correct, fd, gd, xi, N=255) == E.EINVAL
+
+
+def test_check_after_correct(exactz, oracle):
+    f, g, xi = S.make("C2", shape=(16, 16, 40))
+    r = exactz.exactz_correct(f.cuda(), g.cuda(), xi)
+    assert r.status == 0
+    v, _ = exactz.exactz_check(f.cuda(), r.out, xi)
+    assert v == 0
+    marks, cnt = oracle.check(f.numpy(), r.out.cpu().numpy())
+    assert cnt[0] == 0
+
+
+def test_host_entry_matches_device(exactz):
+    f, g, xi = S.make("C1")
+    rd = exactz.exactz_correct(f.cuda(), g.cuda(), xi)
+    rh = exactz.exactz_correct_host(f.pin_memory(), g.pin_memory(), xi)
+    assert rh.iters == rd.iters
+    assert np.array_equal(rh.out.numpy().view(np.uint32), rd.out.cpu().numpy().view(np.uint32))
+
+
+def test_eps_from_relative(exactz):
+    f, _, _ = S.make("C1")
+    e = exactz.exactz_eps_from_relative(f.cuda(), 1e-2)
+    assert e == S.xi_from_rel(f, 1e-2)
+
+
+def test_repeat_bit_identical(exactz):
+    f, g, xi = S.make("C3", shape=(16, 16, 70))
+    a = exactz.exactz_correct(f.cuda(), g.cuda(), xi)
+    b = exactz.exactz_correct(f.cuda(), g.cuda(), xi)
+    assert a.iters == b.iters
+    assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
