@@ -11,7 +11,7 @@ t = time.time()
 f, g, xi = S.make(cfg, device="cuda", shape=shape)
 torch.cuda.synchronize()
 print(cfg, tuple(f.shape), "xi", xi, "gen s", round(time.time() - t, 2), flush=True)
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", "3"))):
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
     r = E.exactz_correct(f, g, xi, stats_cap=10000)
