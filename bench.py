@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py — correction GB/s of the EXaCTz hot path on B200 (BASELINE.json metric).
+
+One *step* = one full correction (exactz_correct: validate, reference of f,
+every detect/edit round until no violation remains) of config C2 — the
+512^3 float32 Nyx-like field at relative eps 1e-3 (BASELINE.json configs[1]) —
+with inputs resident in HBM.  value = 4 * V * n_ranks / (max-over-ranks step
+time), decimal GB/s of field processed (the paper's OT).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
+  python bench.py --impl reference ...   # the CPU oracle arm
+
+N > 1 (torchrun, one rank per GPU): every rank corrects its own replica of the
+workload (scaling "weak"; the sharded z-slab path is reported separately).
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+METRIC = "correction GB/s (field bytes/wall time)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="exactz", choices=["exactz", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=64, help="edge of the oracle's crop")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_name(cfg, f):
+    from synth import fields as S
+    c = S.CONFIGS[cfg]
+    shape = "x".join(str(d) for d in reversed(tuple(f.shape)))
+    return f"{cfg} {c['name']} {shape} float32, rel eps {c['rel']:g}, uniform noise"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def crop(f, g, n):
+    """the centred n^3 (or n x n 2D) crop: a bounded sample of the same field"""
+    if f.dim() == 3 and f.shape[0] > 1:
+        z0, y0, x0 = [(d - min(n, d)) // 2 for d in f.shape]
+        sl = (slice(z0, z0 + min(n, f.shape[0])), slice(y0, y0 + min(n, f.shape[1])),
+              slice(x0, x0 + min(n, f.shape[2])))
+    else:
+        m = n * 8
+        y0, x0 = [(d - min(m, d)) // 2 for d in f.shape[-2:]]
+        sl = (slice(None), slice(y0, y0 + min(m, f.shape[-2])), slice(x0, x0 + min(m, f.shape[-1])))
+    return f[sl].contiguous(), g[sl].contiguous()
+
+
+def oracle_run(f, g, xi):
+    """the CPU oracle, as it stands (single thread), timed with a monotonic clock"""
+    from oracle import oracle as O
+    O.build()
+    fn, gn = f.cpu().numpy(), g.cpu().numpy()
+    t0 = time.perf_counter()
+    r = O.correct(fn, gn, xi, 5)
+    dt = time.perf_counter() - t0
+    return dt, r
+
+
+class Clocks:
+    """nvidia-smi clocks/throttle sampling during the timed region"""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.path = os.path.join("/tmp", f"exactz_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        mp = json.load(open(MEASURED_PEAKS))
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the box's host cores."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import torch
+    from synth import fields as S
+    f, g, xi = S.make(args.config, device="cuda" if torch.cuda.is_available() else "cpu")
+    n = max(16, args.cpu_sample * 3 // 4)
+    fs, gs = crop(f, g, n)
+    fs, gs = fs.cpu(), gs.cpu()
+    times = []
+    iters = None
+    for k in range(args.warmup + args.steps):
+        dt, r = oracle_run(fs, gs, xi)
+        if k >= args.warmup:
+            times.append(dt)
+            iters = r.iters
+    V = fs.numel()
+    ms = 1e3 * sum(times) / len(times)
+    val = 4 * V / (ms / 1e3) / 1e9
+    sample = (f"centred {'x'.join(str(d) for d in reversed(tuple(fs.shape)))} crop of the "
+              f"{args.config} field, xi of the full field; oracle iters {iters}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_name(args.config, f) + " (bounded CPU sample)"},
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": sample, "host_cores": host_cores(), "cpu": cpu_model()},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2604_01397_b200 import _build
+    if rank == 0:
+        _build.build()
+    if ws > 1:
+        dist.barrier()
+    import paper_2604_01397_b200 as E
+    from synth import fields as S
+
+    f, g, xi = S.make(args.config, device=dev)
+    V = f.numel()
+    out = torch.empty_like(g)
+    stream = torch.cuda.current_stream()
+
+    def step(profile=False):
+        return E.exactz_correct(f, g, xi, out=out, flags=E.PROFILE if profile else 0,
+                                stats_cap=100000)
+
+    for _ in range(args.warmup):
+        r0 = step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps, device time, max over ranks
+    clocks = Clocks(local)
+    clocks.start()
+    launches0 = E.kernel_launches()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    results = [step(profile=True) for _ in range(args.steps)]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = E.kernel_launches() - launches0
+    ck = clocks.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    value = 4.0 * V * ws / (ms_step / 1e3) / 1e9
+
+    r = results[-1]
+    iters = r.iters
+    # roofline of the dominant kernel class (CUDA events on the launch stream)
+    agg = {}
+    for res in results:
+        for k, (ms, n, b) in res.kernels.items():
+            a = agg.setdefault(k, [0.0, 0, 0])
+            a[0] += ms
+            a[1] += n
+            a[2] += b
+    dom = max(agg, key=lambda k: agg[k][0])
+    dms, dn, dbytes = agg[dom]
+    peak, peak_src = peaks()
+    achieved = (dbytes / dn) / ((dms / dn) / 1e3) / 1e9 if dn and dms else None
+    share = dms / (ms_step * args.steps)
+    roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                "traffic": None, "peak_source": peak_src,
+                "share_of_step": share,
+                "bytes_per_launch": dbytes / dn if dn else None,
+                "ms_per_launch": dms / dn if dn else None,
+                "classes": {k: {"ms": v[0] / args.steps, "launches": v[1] / args.steps,
+                                "GB/s": (v[2] / (v[0] / 1e3) / 1e9) if v[0] else None}
+                            for k, v in agg.items() if v[1]}}
+    traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        tr = json.load(open(traffic_path))
+        roofline["traffic"] = tr.get(f"k_{dom}", {}).get("bytes_per_launch")
+        roofline["traffic_source"] = tr.get("source")
+    except Exception:
+        pass
+
+    # ---------------- e2e: the C-ABI call with HOST buffers (pinned)
+    fh, gh = f.cpu().pin_memory(), g.cpu().pin_memory()
+    oh = torch.empty_like(gh).pin_memory()
+    E.exactz_correct_host(fh, gh, xi, out=oh)  # warm
+    ke = max(1, min(args.steps, 3))
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ke):
+        E.exactz_correct_host(fh, gh, xi, out=oh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / ke], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    same = bool(torch.equal(oh.view(torch.int32), out.cpu().view(torch.int32)))
+
+    # ---------------- CPU baseline: the oracle on a bounded crop (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        fs, gs = crop(f, g, args.cpu_sample)
+        dt, ro = oracle_run(fs.cpu(), gs.cpu(), xi)
+        cpu = {"value": 4 * fs.numel() / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": (f"centred {'x'.join(str(d) for d in reversed(tuple(fs.shape)))} crop "
+                          f"of the same field, xi of the full field; {dt:.1f} s, "
+                          f"{ro.iters} iters"),
+               "host_cores": host_cores(), "cpu": cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(args.config, f), "V": V, "xi": xi,
+                       "iterations": iters, "status": r.status,
+                       "ms_setup": r.ms_setup, "ms_loop": r.ms_loop,
+                       "l2": f"inputs {4 * V / 1e6:.0f} MB per field > 126 MB L2 (no flush)",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "edit_pct": None},
+            "iterations": iters,
+            "hbm_frac": roofline["frac"],
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": 4.0 * V * ws / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * V, "d2h_bytes_per_step": 4 * V,
+                    "ms_per_step": e2e_ms, "bit_equal_to_device_run": same},
+            "gpu_launches": launches,
+            "clocks": ck,
+            "version": E.version(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -57,9 +57,23 @@ typedef enum {
   EXACTZ_ENOMEM = 8
 } exactz_status;
 
-/* debug flags */
-#define EXACTZ_NO_C2 0x1u /* skip the saddle-ordering rule (C2, R4) */
-#define EXACTZ_NO_C3 0x2u /* skip the event rules (C3, R5/R6) */
+/* flags */
+#define EXACTZ_NO_C2 0x1u   /* debug: skip the saddle-ordering rule (C2, R4) */
+#define EXACTZ_NO_C3 0x2u   /* debug: skip the event rules (C3, R5/R6) */
+#define EXACTZ_PROFILE 0x4u /* time every kernel class with CUDA events on `stream`
+                               (exactz_stats.kernel_ms); results are unchanged */
+
+/* kernel classes reported by EXACTZ_PROFILE */
+enum {
+  EXACTZ_K_VALIDATE = 0, /* bound check (O1) */
+  EXACTZ_K_REFERENCE,    /* reference of f: classify, sort saddles, m1/M1 (O7) */
+  EXACTZ_K_STENCIL,      /* R1-R3 + steepest slots, per round (O8) */
+  EXACTZ_K_SADDLE_ORDER, /* R4 (C2) */
+  EXACTZ_K_EVENTS,       /* R5/R6 (C3) incl. the label walks (O6) */
+  EXACTZ_K_EDIT,         /* count + bounded edits (O9) */
+  EXACTZ_K_LABELS,       /* full label outputs (pointer jumping) */
+  EXACTZ_K_CLASSES = 8
+};
 
 /* One row per CheckConstraints pass (the last row is the clean pass on OK). */
 typedef struct {
@@ -77,6 +91,10 @@ typedef struct {
   uint32_t nrows;          /* out: number of detection passes (may exceed cap) */
   double ms_setup;         /* out: validate + reference setup (CUDA events) */
   double ms_loop;          /* out: all iterations */
+  /* EXACTZ_PROFILE only: per kernel class (EXACTZ_K_*), summed over the call */
+  double kernel_ms[EXACTZ_K_CLASSES];       /* CUDA-event time on `stream` */
+  uint64_t kernel_launches[EXACTZ_K_CLASSES];
+  uint64_t kernel_bytes[EXACTZ_K_CLASSES];  /* algorithmic bytes */
 } exactz_stats;
 
 typedef struct {
@@ -133,6 +151,10 @@ exactz_status exactz_correct_sharded(exactz_comm *comm, const float *f_local,
 
 const char *exactz_strerror(exactz_status s);
 const char *exactz_last_error(void);
+/* Number of this library's own kernels launched by the calling process so far
+ * (diagnostic; library kernels such as CUB's sort are not counted). */
+uint64_t exactz_kernel_launches(void);
+
 /* build identification, e.g. "exactz sm_100a <git-describe>" */
 const char *exactz_version(void);
 

@@ -16,7 +16,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libexactz.so")
 
 OK, EINVAL, EBOUND, ESTUCK, EUNSUPPORTED, ECUDA, ENCCL, ENOMEM = 0, 2, 3, 4, 5, 6, 7, 8
-NO_C2, NO_C3 = 0x1, 0x2
+NO_C2, NO_C3, PROFILE = 0x1, 0x2, 0x4
+KERNEL_CLASSES = ("validate", "reference", "stencil", "saddle_order", "events", "edit", "labels",
+                  "spare")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g;"
@@ -29,7 +31,9 @@ class IterStats(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("rows", C.POINTER(IterStats)), ("cap", C.c_uint32), ("nrows", C.c_uint32),
-                ("ms_setup", C.c_double), ("ms_loop", C.c_double)]
+                ("ms_setup", C.c_double), ("ms_loop", C.c_double),
+                ("kernel_ms", C.c_double * 8), ("kernel_launches", C.c_uint64 * 8),
+                ("kernel_bytes", C.c_uint64 * 8)]
 
 
 class Opts(C.Structure):
@@ -54,6 +58,7 @@ _lib.exactz_strerror.argtypes = [C.c_int]
 _lib.exactz_strerror.restype = C.c_char_p
 _lib.exactz_last_error.restype = C.c_char_p
 _lib.exactz_version.restype = C.c_char_p
+_lib.exactz_kernel_launches.restype = C.c_uint64
 _lib.exactz_nccl_unique_id.argtypes = [_P]
 _lib.exactz_nccl_unique_id.restype = C.c_int
 _lib.exactz_comm_init.argtypes = [_P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
@@ -73,6 +78,11 @@ def version() -> str:
     return _lib.exactz_version().decode()
 
 
+def kernel_launches() -> int:
+    """This library's own kernel launches so far in this process."""
+    return int(_lib.exactz_kernel_launches())
+
+
 def last_error() -> str:
     return _lib.exactz_last_error().decode()
 
@@ -90,6 +100,7 @@ class CorrectResult:
     stats: list            # per detection pass: (V_t, applied, n1..n6)
     ms_setup: float
     ms_loop: float
+    kernels: dict = None   # PROFILE: class -> (ms, launches, algorithmic bytes)
 
 
 def _dims(t) -> C.Array:
@@ -125,7 +136,9 @@ def _opts(N, max_iters, flags, edit_counts, label_min, label_max, stats_cap):
 def _result(status, iters, st, rows):
     n = min(st.nrows, st.cap)
     table = [(r.violations, r.applied, *list(r.n)) for r in rows[:n]] if st.cap else []
-    return CorrectResult(status, iters.value, table, st.ms_setup, st.ms_loop)
+    kern = {KERNEL_CLASSES[k]: (st.kernel_ms[k], int(st.kernel_launches[k]),
+                                int(st.kernel_bytes[k])) for k in range(8)}
+    return CorrectResult(status, iters.value, table, st.ms_setup, st.ms_loop, kern)
 
 
 def exactz_correct(f, g_in, eps: float, out=None, *, N: int = 5, max_iters: int = 0,

@@ -8,6 +8,8 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -69,11 +71,79 @@ static int blocks_for(int64_t n, int threads, int cap = 148 * 16) {
   return (int)(b < 1 ? 1 : b);
 }
 
+static std::atomic<uint64_t> g_launches{0};
+
+// Per-kernel-class CUDA-event timing (EXACTZ_PROFILE).  Events are recorded
+// on the launch stream around each kernel and read at the next host sync.
+struct Prof {
+  bool on = false;
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> pool;
+  std::vector<Rec> pending;
+  double ms[EXACTZ_K_CLASSES] = {};
+  uint64_t launches[EXACTZ_K_CLASSES] = {}, bytes[EXACTZ_K_CLASSES] = {};
+  ~Prof() {
+    for (auto &r : pending) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  void drain() {  // call after a stream sync
+    for (auto &r : pending) {
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, r.a, r.b));
+      ms[r.cls] += t;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    pending.clear();
+  }
+};
+
 struct Ctx {
   cudaStream_t s;
+  Prof prof;
+  // Launch one kernel (or library call) of class `cls`; `ours` counts it as
+  // one of this library's kernels.
+  template <class Fn>
+  void run(int cls, uint64_t bytes, bool ours, Fn fn) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (prof.on) {
+      a = prof.get();
+      CK(cudaEventRecord(a, s));
+    }
+    fn();
+    CK(cudaGetLastError());
+    if (prof.on) {
+      b = prof.get();
+      CK(cudaEventRecord(b, s));
+      prof.pending.push_back({cls, a, b});
+    }
+    if (ours) {
+      prof.launches[cls]++;
+      g_launches++;
+    }
+    prof.bytes[cls] += bytes;
+  }
   GridP G{};
   int64_t V = 0;
-  dim3 sgrid, sblock;
+  dim3 sgrid, sblock;                 // stencil: 32x8 columns, z chunks
+  dim3 rgrid, vblock;                 // persistent row-parallel grid, 128 x-threads
+  int zc = 1;
   unsigned long long *cnt = nullptr;  // device counters
   unsigned long long *hcnt = nullptr; // pinned host mirror
   Arena arena;
@@ -82,22 +152,66 @@ struct Ctx {
     if (hcnt) cudaFreeHost(hcnt);
   }
   void init(const int64_t dims[3]) {
+    keep_pool();
     G.nx = (int)dims[0];
     G.ny = (int)dims[1];
     G.nz = (int)dims[2];
     G.V = (int)V;
+    G.W = (G.nx + 31) / 32;
     for (int s = 0; s < kSlots; ++s)
       G.delta[s] = kOff[s][0] + G.nx * (kOff[s][1] + G.ny * kOff[s][2]);
-    sblock = dim3(128, 1, 1);
-    sgrid = dim3((unsigned)((G.nx + 127) / 128), (unsigned)G.ny, (unsigned)G.nz);
+    // z chunk per stencil CTA: enough CTAs to fill 148 SMs several times over,
+    // few enough halo planes (2 per chunk) to keep re-reads small
+    int64_t cols = (int64_t)((G.nx + TX - 1) / TX) * ((G.ny + TY - 1) / TY);
+    int64_t want = 148 * 24;
+    int64_t z = cols >= want ? G.nz : (G.nz * cols + want - 1) / want;
+    zc = (int)(z < 8 ? 8 : (z > 64 ? 64 : z));
+    if (zc > G.nz) zc = G.nz;
+    sblock = dim3(TX, TY, 1);
+    sgrid = dim3((unsigned)((G.nx + TX - 1) / TX), (unsigned)((G.ny + TY - 1) / TY),
+                 (unsigned)((G.nz + zc - 1) / zc));
+    vblock = dim3(128, 1, 1);
+    {
+      unsigned bx = (unsigned)((G.nx + 127) / 128);
+      if (bx > 8) bx = 8;
+      int64_t rows = (int64_t)G.ny * G.nz, by = (148 * 16 + bx - 1) / bx;
+      rgrid = dim3(bx, (unsigned)(rows < by ? rows : by), 1);
+    }
     cnt = arena.get<unsigned long long>(C_NCOUNTERS);
     CK(cudaMallocHost(&hcnt, C_NCOUNTERS * sizeof(unsigned long long)));
+    upload_lut();
   }
+  // Keep freed stream-ordered memory in the device's default pool between
+  // calls (the default release threshold 0 returns it to the OS at every
+  // sync, making each call re-map its scratch).
+  static void keep_pool() {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  void upload_lut() {
+    static thread_local uint8_t lut[1 << kSlots];
+    static thread_local bool ready = false;
+    if (!ready) {
+      for (uint32_t m = 0; m < (1u << kSlots); ++m) {
+        int nl = link_components_t(m, kLink.adj);
+        int nu = link_components_t(0x3FFFu & ~m, kLink.adj);
+        lut[m] = (uint8_t)(nl | (nu << 4));
+      }
+      ready = true;
+    }
+    CK(cudaMemcpyToSymbolAsync(d_lut, lut, sizeof(lut), 0, cudaMemcpyHostToDevice, s));
+  }
+  size_t mark_words() const { return (size_t)G.ny * G.nz * G.W; }
   void zero() { CK(cudaMemsetAsync(cnt, 0, C_NCOUNTERS * sizeof(unsigned long long), s)); }
   void read() {
     CK(cudaMemcpyAsync(hcnt, cnt, C_NCOUNTERS * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (prof.on) prof.drain();
   }
 };
 
@@ -112,43 +226,64 @@ static exactz_status check_dims(const int64_t dims[3], int64_t *V) {
   return EXACTZ_OK;
 }
 
-// Resolve a pointer forest to its roots (O6).
-static void resolve_labels(Ctx &C, int32_t *lab) {
-  for (int round = 0; round < 64; ++round) {
-    CK(cudaMemsetAsync(&C.cnt[C_CHANGED], 0, sizeof(unsigned long long), C.s));
-    k_jump<<<blocks_for(C.V, 256), 256, 0, C.s>>>(lab, C.V, 8, C.cnt);
-    CK(cudaGetLastError());
-    unsigned long long ch = 0;
-    CK(cudaMemcpyAsync(&ch, &C.cnt[C_CHANGED], sizeof(ch), cudaMemcpyDeviceToHost, C.s));
-    CK(cudaStreamSynchronize(C.s));
-    if (!ch) return;
+// Resolve pointer forests to their roots (O6) by pointer jumping; only for the
+// optional full label outputs.
+static void full_labels(Ctx &C, const uint8_t *slots, int32_t *lab_dn, int32_t *lab_up) {
+  C.run(EXACTZ_K_LABELS, 9 * (uint64_t)C.V, true, [&] {
+    k_slots_to_ptrs<<<blocks_for(C.V, 256, 1 << 30), 256, 0, C.s>>>(slots, lab_dn, lab_up, C.G);
+  });
+  for (int32_t *lab : {lab_dn, lab_up}) {
+    if (!lab) continue;
+    for (int round = 0;; ++round) {
+      if (round > 64) {
+        set_err("full_labels", "pointer jumping did not converge");
+        throw Error{EXACTZ_ECUDA};
+      }
+      CK(cudaMemsetAsync(&C.cnt[C_CHANGED], 0, sizeof(unsigned long long), C.s));
+      C.run(EXACTZ_K_LABELS, 8 * (uint64_t)C.V, true, [&] {
+        k_jump<<<blocks_for(C.V, 256), 256, 0, C.s>>>(lab, C.V, C.cnt);
+      });
+      unsigned long long ch = 0;
+      CK(cudaMemcpyAsync(&ch, &C.cnt[C_CHANGED], sizeof(ch), cudaMemcpyDeviceToHost, C.s));
+      CK(cudaStreamSynchronize(C.s));
+      if (C.prof.on) C.prof.drain();
+      if (!ch) break;
+    }
   }
-  set_err("resolve_labels", "pointer jumping did not converge");
-  throw Error{EXACTZ_ECUDA};
 }
 
 struct Reference {
   uint32_t *ref = nullptr;
-  int32_t *labf_dn = nullptr, *labf_up = nullptr;
   int32_t *S = nullptr, *J = nullptr, *P = nullptr, *m1 = nullptr, *M1 = nullptr;
   int nS = 0, nJ = 0, nP = 0;
 };
+
+template <bool SPLIT, bool FROM_REF>
+static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, const uint8_t *slots,
+                          const uint32_t *ref, int32_t *ext, uint32_t *marks) {
+  if (n <= 0) return;
+  int64_t threads = (int64_t)n * 16;
+  // algorithmic bytes: per saddle its id, its value, 14 link values, the
+  // reached extrema's values and ids
+  C.run(FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS, 128ull * n, true, [&] {
+    k_events<SPLIT, FROM_REF><<<(unsigned)((threads + 255) / 256), 256, 0, C.s>>>(
+        h, sl, n, slots, ref, ext, marks, C.G, C.cnt);
+  });
+}
 
 // O7: reference topology of f, computed once per call.
 static void build_reference(Ctx &C, const float *f, Reference &R) {
   int64_t V = C.V;
   R.ref = C.arena.get<uint32_t>(V);
-  R.labf_dn = C.arena.get<int32_t>(V);
-  R.labf_up = C.arena.get<int32_t>(V);
   uint64_t *keys = C.arena.get<uint64_t>(V);
   C.zero();
-  k_reference<<<C.sgrid, C.sblock, 0, C.s>>>(f, C.G, R.ref, R.labf_dn, R.labf_up, keys, C.cnt);
-  CK(cudaGetLastError());
+  C.run(EXACTZ_K_REFERENCE, 8 * (uint64_t)V, true,
+        [&] { k_reference<<<C.rgrid, C.vblock, 0, C.s>>>(f, C.G, R.ref, keys, C.cnt); });
   C.read();
   R.nS = (int)C.hcnt[C_NSADDLE];
-  resolve_labels(C, R.labf_dn);
-  resolve_labels(C, R.labf_up);
-  // saddles sorted by the SoS key of f
+  // S: all saddles sorted by the SoS key of f.  J, P: join / split
+  // saddles in index (spatial) order, so that consecutive event checks walk
+  // nearby integral paths (L1/L2 reuse); their order is otherwise irrelevant.
   uint64_t *sorted = C.arena.get<uint64_t>(R.nS);
   R.S = C.arena.get<int32_t>(R.nS);
   R.J = C.arena.get<int32_t>(R.nS);
@@ -156,92 +291,81 @@ static void build_reference(Ctx &C, const float *f, Reference &R) {
   int *nsel = C.arena.get<int>(2);
   if (R.nS > 0) {
     size_t tb = 0, tb2 = 0, tb3 = 0;
+    cub::CountingInputIterator<int32_t> ids(0);
     CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, R.nS, 0, 64, C.s));
-    CK(cub::DeviceSelect::If(nullptr, tb2, R.S, R.J, nsel, R.nS, IsJoin{R.ref}, C.s));
-    CK(cub::DeviceSelect::If(nullptr, tb3, R.S, R.P, nsel + 1, R.nS, IsSplit{R.ref}, C.s));
+    CK(cub::DeviceSelect::If(nullptr, tb2, ids, R.J, nsel, (int)V, IsJoin{R.ref}, C.s));
+    CK(cub::DeviceSelect::If(nullptr, tb3, ids, R.P, nsel + 1, (int)V, IsSplit{R.ref}, C.s));
     size_t tmax = tb > tb2 ? tb : tb2;
     tmax = tmax > tb3 ? tmax : tb3;
     void *tmp = C.arena.get<uint8_t>(tmax);
-    CK(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, R.nS, 0, 64, C.s));
-    k_keys_to_ids<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(sorted, R.S, R.nS);
-    CK(cudaGetLastError());
-    CK(cub::DeviceSelect::If(tmp, tb2, R.S, R.J, nsel, R.nS, IsJoin{R.ref}, C.s));
-    CK(cub::DeviceSelect::If(tmp, tb3, R.S, R.P, nsel + 1, R.nS, IsSplit{R.ref}, C.s));
+    C.run(EXACTZ_K_REFERENCE, 32ull * R.nS, false, [&] {
+      CK(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, R.nS, 0, 64, C.s));
+    });
+    C.run(EXACTZ_K_REFERENCE, 12ull * R.nS, true, [&] {
+      k_keys_to_ids<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(sorted, R.S, R.nS);
+    });
+    C.run(EXACTZ_K_REFERENCE, 8ull * V, false, [&] {
+      CK(cub::DeviceSelect::If(tmp, tb2, ids, R.J, nsel, (int)V, IsJoin{R.ref}, C.s));
+      CK(cub::DeviceSelect::If(tmp, tb3, ids, R.P, nsel + 1, (int)V, IsSplit{R.ref}, C.s));
+    });
     int h[2];
     CK(cudaMemcpyAsync(h, nsel, sizeof(h), cudaMemcpyDeviceToHost, C.s));
     CK(cudaStreamSynchronize(C.s));
+    if (C.prof.on) C.prof.drain();
     R.nJ = h[0];
     R.nP = h[1];
   }
   R.m1 = C.arena.get<int32_t>(R.nJ);
   R.M1 = C.arena.get<int32_t>(R.nP);
-  if (R.nJ)
-    k_event_reference<<<blocks_for(R.nJ, 128, 1 << 30), 128, 0, C.s>>>(
-        f, R.ref, R.labf_dn, R.J, R.nJ, 1, R.m1, C.G);
-  if (R.nP)
-    k_event_reference<<<blocks_for(R.nP, 128, 1 << 30), 128, 0, C.s>>>(
-        f, R.ref, R.labf_up, R.P, R.nP, 0, R.M1, C.G);
-  CK(cudaGetLastError());
+  // m1 / M1 by walking f's steepest paths from each saddle's link
+  launch_events<false, true>(C, f, R.J, R.nJ, nullptr, R.ref, R.m1, nullptr);
+  launch_events<true, true>(C, f, R.P, R.nP, nullptr, R.ref, R.M1, nullptr);
 }
 
 struct PassOut {
   unsigned long long vt, applied, n[6];
-  bool ptr_mismatch;
 };
 
 // One CheckConstraints pass on g (O8) followed by the count and, when
-// do_edit, the bounded edits (O9).  lab_dn/lab_up receive the g pointer
-// forests (resolved when they differ from f's).
+// do_edit, the bounded edits (O9).  slots receives g's steepest slots.
 static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float *g, uint8_t *c,
-                               uint8_t *mark, int32_t *lab_dn, int32_t *lab_up, float xi,
-                               float delta, int N, uint32_t flags, bool do_edit,
-                               const int32_t **lab_used_dn, const int32_t **lab_used_up) {
+                               uint32_t *marks, uint8_t *slots, float xi, float delta, int N,
+                               uint32_t flags, bool do_edit) {
   bool c3 = !(flags & EXACTZ_NO_C3);
   C.zero();
-  k_stencil<<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, mark, lab_dn, lab_up, 1, C.G, C.cnt);
-  CK(cudaGetLastError());
-  if (!(flags & EXACTZ_NO_C2) && R.nS > 1)
-    k_saddle_order<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(g, R.S, R.nS, mark, C.cnt);
-  CK(cudaGetLastError());
-  C.read();
-  bool mismatch_dn = C.hcnt[C_N1 + 1] != 0, mismatch_up = C.hcnt[C_N1 + 0] != 0;
-  // Labels of g equal those of f exactly when no steepest pointer differs.
-  const int32_t *ldn = R.labf_dn, *lup = R.labf_up;
-  if (mismatch_dn) {
-    resolve_labels(C, lab_dn);
-    ldn = lab_dn;
-  }
-  if (mismatch_up) {
-    resolve_labels(C, lab_up);
-    lup = lab_up;
+  // algorithmic bytes per vertex: g 4 + ref 4 read, slots 1 + mark bits 1/8
+  // written
+  C.run(EXACTZ_K_STENCIL, (uint64_t)C.V * 73 / 8, true, [&] {
+    k_stencil<<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, C.G, C.zc, C.cnt);
+  });
+  if (!(flags & EXACTZ_NO_C2) && R.nS > 1) {
+    C.run(EXACTZ_K_SADDLE_ORDER, 8ull * R.nS, true, [&] {
+      k_saddle_order<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(g, R.S, R.nS, marks, C.G,
+                                                                      C.cnt);
+    });
   }
   if (c3) {
-    if (R.nJ)
-      k_events<<<blocks_for(R.nJ, 128, 1 << 30), 128, 0, C.s>>>(g, R.J, R.nJ, ldn, R.m1, 0, mark,
-                                                                C.G, C.cnt);
-    if (R.nP)
-      k_events<<<blocks_for(R.nP, 128, 1 << 30), 128, 0, C.s>>>(g, R.P, R.nP, lup, R.M1, 1, mark,
-                                                                C.G, C.cnt);
-    CK(cudaGetLastError());
+    launch_events<false, false>(C, g, R.J, R.nJ, slots, R.ref, R.m1, marks);
+    launch_events<true, false>(C, g, R.P, R.nP, slots, R.ref, R.M1, marks);
   }
-  k_count_edit<<<blocks_for(C.V, 256), 256, 0, C.s>>>(g, c, mark, f, C.V, xi, delta, N,
-                                                       do_edit ? 1 : 0, C.cnt);
-  CK(cudaGetLastError());
+  // bytes: mark words read (the per-edit 14 B are added once V_t is known)
+  C.run(EXACTZ_K_EDIT, (uint64_t)C.V / 8, true, [&] {
+    k_count_edit<<<148 * 8, 256, 0, C.s>>>(g, c, marks, f, C.G, xi, delta, N, do_edit ? 1 : 0,
+                                           C.cnt);
+  });
   C.read();
   PassOut o;
   o.vt = C.hcnt[C_VT];
   o.applied = C.hcnt[C_APPLIED];
+  C.prof.bytes[EXACTZ_K_EDIT] += 14ull * o.applied;  // f, g, c read; g, c written
   for (int k = 0; k < 6; ++k) o.n[k] = C.hcnt[C_N1 + k];
-  o.ptr_mismatch = mismatch_dn || mismatch_up;
-  if (lab_used_dn) *lab_used_dn = ldn;
-  if (lab_used_up) *lab_used_up = lup;
   return o;
 }
 
 static void validate_inputs(Ctx &C, const float *f, const float *g, float xi) {
   C.zero();
-  k_validate<<<blocks_for(C.V, 256), 256, 0, C.s>>>(f, g, C.V, xi, C.cnt);
-  CK(cudaGetLastError());
+  C.run(EXACTZ_K_VALIDATE, 8 * (uint64_t)C.V, true,
+        [&] { k_validate<<<blocks_for(C.V, 256), 256, 0, C.s>>>(f, g, C.V, xi, C.cnt); });
   C.read();
   if (C.hcnt[C_BAD_NF]) {
     set_err("validate", "non-finite value in f or g");
@@ -268,6 +392,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
 
   Ctx C(s);
   C.V = V;
+  C.prof.on = (flags & EXACTZ_PROFILE) != 0;
   C.init(dims);
   cudaEvent_t e0, e1, e2;
   CK(cudaEventCreate(&e0));
@@ -279,20 +404,18 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   Reference R;
   build_reference(C, f, R);
   uint8_t *c = (opts && opts->edit_counts) ? opts->edit_counts : C.arena.get<uint8_t>(V);
-  uint8_t *mark = C.arena.get<uint8_t>(V);
-  int32_t *lab_dn = C.arena.get<int32_t>(V), *lab_up = C.arena.get<int32_t>(V);
+  uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
+  uint8_t *slots = C.arena.get<uint8_t>(V);
   CK(cudaMemsetAsync(c, 0, V, s));
-  CK(cudaMemsetAsync(mark, 0, V, s));
+  CK(cudaMemsetAsync(marks, 0, C.mark_words() * sizeof(uint32_t), s));
   CK(cudaEventRecord(e1, s));
 
   const float delta = eps / (float)N;  // Delta = RN(xi / N)
   uint32_t it = 0, rows = 0;
   exactz_status st = EXACTZ_OK;
-  const int32_t *ldn = R.labf_dn, *lup = R.labf_up;
   for (;;) {
     bool may_edit = !(max_iters && it >= max_iters);
-    PassOut o = detect_and_edit(C, R, f, out, c, mark, lab_dn, lab_up, eps, delta, N, flags,
-                                may_edit, &ldn, &lup);
+    PassOut o = detect_and_edit(C, R, f, out, c, marks, slots, eps, delta, N, flags, may_edit);
     if (stats && stats->rows && rows < stats->cap) {
       exactz_iter_stats &r = stats->rows[rows];
       r.violations = o.vt;
@@ -308,11 +431,13 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     ++it;
   }
   CK(cudaEventRecord(e2, s));
-  // labels of the final field: the last pass ran on it (no edit followed)
-  if (opts && opts->label_min)
-    CK(cudaMemcpyAsync(opts->label_min, ldn, V * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-  if (opts && opts->label_max)
-    CK(cudaMemcpyAsync(opts->label_max, lup, V * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  // labels of the final field: the last pass ran on it (no edit followed), so
+  // `slots` holds its steepest pointers
+  if (opts && (opts->label_min || opts->label_max)) {
+    int32_t *ld = opts->label_min ? opts->label_min : C.arena.get<int32_t>(V);
+    int32_t *lu = opts->label_max ? opts->label_max : C.arena.get<int32_t>(V);
+    full_labels(C, slots, ld, lu);
+  }
   CK(cudaStreamSynchronize(s));
   if (stats) {
     float a = 0, b = 0;
@@ -321,6 +446,11 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     stats->ms_setup = a;
     stats->ms_loop = b;
     stats->nrows = rows;
+    for (int k = 0; k < EXACTZ_K_CLASSES; ++k) {
+      stats->kernel_ms[k] = C.prof.ms[k];
+      stats->kernel_launches[k] = C.prof.launches[k];
+      stats->kernel_bytes[k] = C.prof.bytes[k];
+    }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -404,11 +534,11 @@ exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3]
     validate_inputs(C, f, g, eps_abs);
     Reference R;
     build_reference(C, f, R);
-    uint8_t *mark = C.arena.get<uint8_t>(V);
-    int32_t *lab_dn = C.arena.get<int32_t>(V), *lab_up = C.arena.get<int32_t>(V);
-    CK(cudaMemsetAsync(mark, 0, V, s));
-    PassOut o = detect_and_edit(C, R, f, const_cast<float *>(g), nullptr, mark, lab_dn, lab_up,
-                                eps_abs, 0.0f, 5, flags, false, nullptr, nullptr);
+    uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
+    uint8_t *slots = C.arena.get<uint8_t>(V);
+    CK(cudaMemsetAsync(marks, 0, C.mark_words() * sizeof(uint32_t), s));
+    PassOut o = detect_and_edit(C, R, f, const_cast<float *>(g), nullptr, marks, slots, eps_abs,
+                                0.0f, 5, flags, false);
     *violations = o.vt;
     if (row) {
       row->violations = o.vt;
@@ -431,6 +561,7 @@ exactz_status exactz_eps_from_relative(const float *f, int64_t n, double rel, fl
     init[C_KEYMIN] = 0xffffffffull;
     CK(cudaMemcpyAsync(cnt, init, sizeof(init), cudaMemcpyHostToDevice, s));
     k_minmax<<<blocks_for(n, 256), 256, 0, s>>>(f, n, cnt);
+    g_launches++;
     CK(cudaGetLastError());
     unsigned long long h[C_NCOUNTERS];
     CK(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -487,6 +618,8 @@ const char *exactz_strerror(exactz_status s) {
 }
 
 const char *exactz_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t exactz_kernel_launches(void) { return g_launches.load(); }
 
 const char *exactz_version(void) { return "exactz sm_100a " EXACTZ_GIT; }
 

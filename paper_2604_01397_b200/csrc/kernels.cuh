@@ -1,12 +1,12 @@
 // kernels.cuh — sm_100a kernels of the EXaCTz correction loop.
 //
 // Every kernel is deterministic regardless of thread order:
-//  * detection reads a snapshot of g (Jacobi, amb-15) and only ever stores
-//    the byte 1 into mark[] (idempotent; a vertex is edited at most once per
+//  * detection reads a snapshot of g (Jacobi, amb-15) and only ever ORs bits
+//    into the mark bitmap (idempotent; a vertex is edited at most once per
 //    round);
 //  * counts are integer atomics of warp-reduced partial sums;
-//  * label pointer jumping only ever replaces a pointer by one of its
-//    ancestors, so its fixpoint (the forest roots) is unique;
+//  * labels are the unique terminus of a steepest path (walks, or pointer
+//    jumping whose fixpoint is unique);
 //  * the edit is a pure function of (g_i, c_i, f_i).
 // IEEE float semantics are kept exact: no fast-math, explicit compare-select
 // (never fminf/fmaxf, whose result for -0/+0 is unspecified), __fsub_ru /
@@ -19,6 +19,13 @@
 namespace exz {
 
 __constant__ LinkTables c_link = kLink;
+// Slot s decodes arithmetically (no table lookups with divergent indices):
+// b = s - 6 for s >= 7, 7 - s for s < 7; offset = sign * (b&1, (b>>1)&1, b>>2).
+__host__ __device__ __forceinline__ int slot_bits(int s) { return s >= 7 ? s - 6 : 7 - s; }
+__host__ __device__ __forceinline__ int slot_sign(int s) { return s >= 7 ? 1 : -1; }
+
+// (nlc | nuc << 4) of every interior lower mask (slot order), built on the host
+__device__ uint8_t d_lut[1 << kSlots];
 
 enum Counter {
   C_VT = 0,       // distinct marked vertices
@@ -35,6 +42,7 @@ enum Counter {
 
 struct GridP {
   int nx, ny, nz, V;
+  int W;              // 32-bit words per row of the mark bitmap, ceil(nx/32)
   int delta[kSlots];  // linear offset of each slot
 };
 
@@ -65,20 +73,21 @@ __device__ __forceinline__ uint32_t valid_mask(int x, int y, int z, const GridP 
 }
 
 // Number of connected components of the link graph induced on `set`
-// (bit-parallel flood fill; O4).
-__device__ __forceinline__ uint32_t link_expand(uint32_t r) {
+// (bit-parallel flood fill; O4).  Used for boundary vertices and to build the
+// interior LUT.
+__host__ __device__ __forceinline__ uint32_t link_expand(uint32_t r, const uint16_t *adj) {
   uint32_t n = r;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s)
-    if (r & (1u << s)) n |= c_link.adj[s];
+    if (r & (1u << s)) n |= adj[s];
   return n;
 }
-__device__ __noinline__ int link_components(uint32_t set) {
+__host__ __device__ inline int link_components_t(uint32_t set, const uint16_t *adj) {
   int n = 0;
   while (set) {
     uint32_t r = set & (0u - set);
     for (;;) {
-      uint32_t r2 = link_expand(r) & set;
+      uint32_t r2 = link_expand(r, adj) & set;
       if (r2 == r) break;
       r = r2;
     }
@@ -87,46 +96,68 @@ __device__ __noinline__ int link_components(uint32_t set) {
   }
   return n;
 }
+__device__ __noinline__ int link_components(uint32_t set) {
+  return link_components_t(set, c_link.adj);
+}
+
+// (nlc, nuc) of a vertex with lower mask `lower` and valid mask `valid`.
+__device__ __forceinline__ void link_type(uint32_t lower, uint32_t valid, int &nl, int &nu) {
+  if (valid == 0x3FFFu) {
+    uint32_t t = d_lut[lower];
+    nl = t & 15;
+    nu = t >> 4;
+  } else {
+    nl = link_components(lower);
+    nu = link_components(valid & ~lower);
+  }
+}
 
 struct Star {
   uint32_t lower;  // slot s set <=> neighbour s <_h i (SoS)
   int dn, up;      // SoS argmin / argmax of the closed star (slot, 14 = self)
 };
 
-// Closed-star evaluation of vertex i of field h (O4 lower mask, O5 steepest).
-__device__ __forceinline__ Star eval_star(const float *__restrict__ h, int i, uint32_t valid,
-                                          const GridP &G) {
-  const float hc = h[i];
-  float v[kSlots];
-#pragma unroll
-  for (int s = 0; s < kSlots; ++s) v[s] = (valid & (1u << s)) ? h[i + G.delta[s]] : 0.0f;
+// Closed-star evaluation (O4 lower mask, O5 steepest) from the 14 neighbour
+// values v[] (slot order) and the centre hc.  SoS by static slot direction:
+// candidates are visited in ascending index order (slots 0..6, the centre,
+// slots 7..13) with a strict compare for the argmin (first minimum = smallest
+// index wins a tie) and a non-strict one for the argmax (last maximum =
+// largest index wins).  Missing neighbours hold NaN, for which every compare
+// is false: they are never lower, never the argmin, never the argmax.
+__device__ __forceinline__ Star eval_values(const float (&v)[kSlots], float hc) {
   Star st;
   st.lower = 0;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
     bool lo = (s < 7) ? (v[s] <= hc) : (v[s] < hc);
-    if ((valid & (1u << s)) && lo) st.lower |= 1u << s;
+    st.lower |= lo ? (1u << s) : 0u;
   }
-  // argmin in ascending index order, strict compare: the first minimum wins
-  int dn = -1, up = -1;
-  float dv = 0.0f, uv = 0.0f;
+  int dn = kSelf, up = kSelf;
+  float dv = __int_as_float(0x7f800000), uv = -__int_as_float(0x7f800000);  // +inf, -inf
 #pragma unroll
-  for (int s = 0; s < 7; ++s)
-    if (valid & (1u << s)) {
-      if (dn < 0 || v[s] < dv) { dn = s; dv = v[s]; }
-      if (up < 0 || v[s] >= uv) { up = s; uv = v[s]; }
-    }
-  if (dn < 0 || hc < dv) { dn = kSelf; dv = hc; }
-  if (up < 0 || hc >= uv) { up = kSelf; uv = hc; }
+  for (int s = 0; s < 7; ++s) {
+    if (v[s] < dv) { dn = s; dv = v[s]; }
+    if (v[s] >= uv) { up = s; uv = v[s]; }
+  }
+  if (hc < dv) { dn = kSelf; dv = hc; }
+  if (hc >= uv) { up = kSelf; uv = hc; }
 #pragma unroll
-  for (int s = 7; s < kSlots; ++s)
-    if (valid & (1u << s)) {
-      if (v[s] < dv) { dn = s; dv = v[s]; }
-      if (v[s] >= uv) { up = s; uv = v[s]; }
-    }
+  for (int s = 7; s < kSlots; ++s) {
+    if (v[s] < dv) { dn = s; dv = v[s]; }
+    if (v[s] >= uv) { up = s; uv = v[s]; }
+  }
   st.dn = dn;
   st.up = up;
   return st;
+}
+
+__device__ __forceinline__ Star eval_star(const float *__restrict__ h, int i, uint32_t valid,
+                                          const GridP &G) {
+  float v[kSlots];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s)
+    v[s] = (valid & (1u << s)) ? h[i + G.delta[s]] : __int_as_float(0x7fc00000);
+  return eval_values(v, h[i]);
 }
 
 __device__ __forceinline__ int slot_target(int i, int slot, const GridP &G) {
@@ -143,6 +174,17 @@ __device__ __forceinline__ uint32_t ordered_key(float v) {
   uint32_t b = __float_as_uint(v);
   if (b == 0x80000000u) b = 0u;
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// mark bitmap: row-padded, bit x of word row*W + x/32 (row = y + ny*z)
+__device__ __forceinline__ void mark_vertex(uint32_t *marks, int v, const GridP &G) {
+  int x = v % G.nx, row = v / G.nx;
+  atomicOr(&marks[(size_t)row * G.W + (x >> 5)], 1u << (x & 31));
+}
+
+__device__ __forceinline__ bool sos_less_g(const float *h, int u, int v) {
+  float a = h[u], b = h[v];
+  return a < b || (a == b && u < v);
 }
 
 // ---------------------------------------------------------------- validate (O1)
@@ -164,32 +206,37 @@ __global__ void k_validate(const float *__restrict__ f, const float *__restrict_
 }
 
 // ------------------------------------------------------ reference of f (O7)
-// One thread per vertex: classification, steepest slots, ref word, the
-// pointer forests of f (into labf_dn / labf_up, resolved later by jumping)
-// and the SoS keys of the saddles (sorted later).
-__global__ void __launch_bounds__(128) k_reference(const float *__restrict__ f, GridP G,
-                                                   uint32_t *__restrict__ ref, int32_t *labf_dn,
-                                                   int32_t *labf_up, uint64_t *saddle_keys,
-                                                   unsigned long long *cnt) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, z = blockIdx.z;
-  if (x >= G.nx) return;
+// Classification, steepest slots and the ref word of vertex (x, y, z) of f;
+// SoS keys of the saddles are appended (sorted later).
+__device__ __forceinline__ void reference_vertex(const float *__restrict__ f, const GridP &G,
+                                                 uint32_t *__restrict__ ref,
+                                                 uint64_t *saddle_keys, unsigned long long *cnt,
+                                                 int x, int y, int z) {
   int i = x + G.nx * (y + G.ny * z);
   uint32_t valid = valid_mask(x, y, z, G);
   Star st = eval_star(f, i, valid, G);
-  int nlc = link_components(st.lower);
-  int nuc = link_components(valid & ~st.lower);
+  int nlc, nuc;
+  link_type(st.lower, valid, nlc, nuc);
   bool isext = (nlc == 0) || (nuc == 0);
   bool sad = !isext && (nlc >= 2 || nuc >= 2);
   bool join = sad && nlc >= 2, split = sad && nuc >= 2;
   ref[i] = st.lower | ((uint32_t)st.dn << 14) | ((uint32_t)st.up << 18) | ((uint32_t)nlc << 22) |
            ((uint32_t)nuc << 25) | ((uint32_t)sad << 28) | ((uint32_t)join << 29) |
            ((uint32_t)split << 30);
-  labf_dn[i] = slot_target(i, st.dn, G);
-  labf_up[i] = slot_target(i, st.up, G);
   if (sad) {
     unsigned long long k = atomicAdd(&cnt[C_NSADDLE], 1ull);
     saddle_keys[k] = ((uint64_t)ordered_key(f[i]) << 32) | (uint32_t)i;
   }
+}
+
+// Persistent 2D grid over rows (y + ny*z) and x.
+__global__ void __launch_bounds__(128) k_reference(const float *__restrict__ f, GridP G,
+                                                   uint32_t *__restrict__ ref,
+                                                   uint64_t *saddle_keys,
+                                                   unsigned long long *cnt) {
+  for (int row = blockIdx.y; row < G.ny * G.nz; row += gridDim.y)
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < G.nx; x += gridDim.x * blockDim.x)
+      reference_vertex(f, G, ref, saddle_keys, cnt, x, row % G.ny, row / G.ny);
 }
 
 __global__ void k_keys_to_ids(const uint64_t *__restrict__ keys, int32_t *ids, int n) {
@@ -206,101 +253,166 @@ struct IsSplit {
   __device__ __forceinline__ bool operator()(const int32_t &s) const { return ref_split(ref[s]); }
 };
 
-__device__ __forceinline__ bool sos_less_g(const float *h, int u, int v) {
-  float a = h[u], b = h[v];
-  return a < b || (a == b && u < v);
-}
-
-// m1(s): the <_f-largest minimum reached from the f-lower link of a join
-// saddle; M1(s): the <_f-smallest maximum reached from the upper link of a
-// split saddle.
-__global__ void k_event_reference(const float *__restrict__ f, const uint32_t *__restrict__ ref,
-                                  const int32_t *__restrict__ lab, const int32_t *__restrict__ sl,
-                                  int n, int want_max, int32_t *out, GridP G) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  int s = sl[k];
-  int x = s % G.nx, y = (s / G.nx) % G.ny, z = s / (G.nx * G.ny);
-  uint32_t valid = valid_mask(x, y, z, G);
-  uint32_t flow = ref_flow(ref[s]);
-  uint32_t set = want_max ? flow : (valid & ~flow);
-  int best = -1;
-  for (uint32_t m = set; m; m &= m - 1) {
-    int slot = __ffs(m) - 1;
-    int e = lab[s + G.delta[slot]];
-    if (best < 0 || (want_max ? sos_less_g(f, best, e) : sos_less_g(f, e, best))) best = e;
-  }
-  out[k] = best;
-}
-
-// --------------------------------------------------- pointer jumping (O6)
-// lab[] holds, for every vertex, a pointer to an ancestor in its steepest
-// forest; one round replaces it by an ancestor up to 2^hops further.  Reads
-// may see pointers other threads already advanced (still ancestors), which
-// only speeds convergence; the fixpoint (roots) is unique.
-__global__ void k_jump(int32_t *lab, int64_t V, int hops, unsigned long long *cnt) {
-  unsigned changed = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int w = lab[i];
-    int w2 = lab[w];
-    if (w2 == w) continue;
-    for (int h = 0; h < hops; ++h) {
-      int w3 = lab[w2];
-      if (w3 == w2) break;
-      w2 = w3;
-    }
-    lab[i] = w2;
-    changed = 1;
-  }
-  if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) atomicOr(&cnt[C_CHANGED], 1ull);
-}
-
 // ------------------------------------------------------- detection (O8)
-// R1, R2, R3 at every vertex from its closed star in g and its ref word;
-// writes the g pointer forests for the labels when `ptrs` is set.
-__global__ void __launch_bounds__(128) k_stencil(const float *__restrict__ g,
-                                                 const uint32_t *__restrict__ ref,
-                                                 uint8_t *mark, int32_t *pdn, int32_t *pup,
-                                                 int ptrs, GridP G, unsigned long long *cnt) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, z = blockIdx.z;
-  unsigned n1 = 0, n2 = 0, n3 = 0;
-  if (x < G.nx) {
-    int i = x + G.nx * (y + G.ny * z);
-    uint32_t valid = valid_mask(x, y, z, G);
-    Star st = eval_star(g, i, valid, G);
-    uint32_t r = ref[i];
-    // R1: the g-largest neighbour is an impostor -> decrease it
-    if (st.up != ref_up(r)) {
-      mark[slot_target(i, st.up, G)] = 1;
-      n1 = 1;
-    }
-    // R2: the g-smallest neighbour changed -> decrease the true N_min
-    if (st.dn != ref_dn(r)) {
-      mark[slot_target(i, ref_dn(r), G)] = 1;
-      n2 = 1;
-    }
-    // R3 (amb-7, amb-8)
-    uint32_t flow = ref_flow(r);
-    uint32_t flip = st.lower ^ flow;
-    if (flip) {
-      bool apply = ref_saddle(r);
-      if (!apply) {
-        int nl = link_components(st.lower);
-        int nu = link_components(valid & ~st.lower);
-        apply = (nl != ref_nlc(r)) || (nu != ref_nuc(r));
-      }
-      if (apply) {
-        n3 = __popc(flip);
-        for (uint32_t m = flip & flow; m; m &= m - 1) mark[i + G.delta[__ffs(m) - 1]] = 1;
-        if (flip & ~flow) mark[i] = 1;
-      }
-    }
-    if (ptrs) {
-      pdn[i] = slot_target(i, st.dn, G);
-      pup[i] = slot_target(i, st.up, G);
+// Stencil tile: 32 (x) x 8 (y) columns per CTA, marching along z through a
+// chunk of planes.  g planes z-1 .. z+2 live in a 4-deep shared-memory ring
+// with a 1-vertex halo; plane z+2 is prefetched into registers while plane z
+// is evaluated.  Marks are ORed into a shared ring of byte planes and flushed
+// to the global bitmap once complete: interior rows as one warp-ballot word,
+// halo cells as single-bit atomics.
+constexpr int TX = 32, TY = 8, NT = TX * TY;
+constexpr int SX = TX + 2, SY = TY + 2, SP = SX * SY;  // 340 cells per plane
+constexpr int PERIM = 2 * SX + 2 * TY;                 // 84 halo cells per plane
+
+__device__ __forceinline__ void perim_cell(int t, int &ly, int &lx) {
+  if (t < SX) { ly = 0; lx = t; }
+  else if (t < 2 * SX) { ly = SY - 1; lx = t - SX; }
+  else if (t < 2 * SX + TY) { ly = 1 + (t - 2 * SX); lx = 0; }
+  else { ly = 1 + (t - 2 * SX - TY); lx = SX - 1; }
+}
+
+// Plane p of the tile with its halo into registers (2 cells per thread);
+// cells outside the domain (or a plane outside [0, nz)) read as NaN.
+__device__ __forceinline__ void load_plane_regs(const float *__restrict__ g, int p, int x0, int y0,
+                                                const GridP &G, float (&r)[2]) {
+  const int tid = threadIdx.y * TX + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    int c = tid + k * NT;
+    r[k] = __int_as_float(0x7fc00000);
+    if (c < SP && p >= 0 && p < G.nz) {
+      int ly = c / SX, lx = c - ly * SX;
+      int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+      if (gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny)
+        r[k] = g[gx + (size_t)G.nx * (gy + (size_t)G.ny * p)];
     }
   }
+}
+__device__ __forceinline__ void store_plane_regs(float *sg, const float (&r)[2]) {
+  const int tid = threadIdx.y * TX + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    int c = tid + k * NT;
+    if (c < SP) sg[c] = r[k];
+  }
+}
+
+// flush one plane of shared marks into the global bitmap
+__device__ __forceinline__ void flush_plane(uint32_t *__restrict__ marks, const uint8_t *sm, int p,
+                                            int x0, int y0, bool interior, const GridP &G) {
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  if (interior) {
+    int gx = x0 + threadIdx.x, gy = y0 + threadIdx.y;
+    bool bit = sm[(threadIdx.y + 1) * SX + threadIdx.x + 1] && gx < G.nx && gy < G.ny;
+    uint32_t w = __ballot_sync(0xffffffffu, bit);
+    if (threadIdx.x == 0 && w)
+      atomicOr(&marks[(size_t)(gy + G.ny * p) * G.W + (x0 >> 5)], w);
+    if (tid < PERIM) {
+      int ly, lx;
+      perim_cell(tid, ly, lx);
+      int hx = x0 - 1 + lx, hy = y0 - 1 + ly;
+      if (sm[ly * SX + lx] && hx >= 0 && hx < G.nx && hy >= 0 && hy < G.ny)
+        atomicOr(&marks[(size_t)(hy + G.ny * p) * G.W + (hx >> 5)], 1u << (hx & 31));
+    }
+  } else {
+    for (int c = tid; c < SP; c += NT) {
+      int ly = c / SX, lx = c - ly * SX;
+      int hx = x0 - 1 + lx, hy = y0 - 1 + ly;
+      if (sm[c] && hx >= 0 && hx < G.nx && hy >= 0 && hy < G.ny)
+        atomicOr(&marks[(size_t)(hy + G.ny * p) * G.W + (hx >> 5)], 1u << (hx & 31));
+    }
+  }
+}
+
+// R1, R2, R3 at every vertex from its closed star in g and its ref word;
+// writes the packed steepest slots (dn | up << 4) used by the label walks.
+__global__ void __launch_bounds__(NT) k_stencil(const float *__restrict__ g,
+                                                const uint32_t *__restrict__ ref,
+                                                uint32_t *__restrict__ marks,
+                                                uint8_t *__restrict__ slots, GridP G, int zc,
+                                                unsigned long long *cnt) {
+  __shared__ float sg[4][SP];
+  __shared__ uint8_t sm[4][SP];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, G.nz);
+  const int x = x0 + tx, y = y0 + ty;
+  const bool inside = x < G.nx && y < G.ny;
+  const int c = (ty + 1) * SX + tx + 1;
+  unsigned n1 = 0, n2 = 0, n3 = 0;
+
+  {  // prologue: planes z0-1, z0, z0+1 (NaN outside the domain), cleared marks
+    float r[2];
+    for (int p = z0 - 1; p <= z0 + 1; ++p) {
+      load_plane_regs(g, p, x0, y0, G, r);
+      store_plane_regs(sg[p & 3], r);
+    }
+    for (int k = tid; k < 4 * SP; k += NT) (&sm[0][0])[k] = 0;
+  }
+  __syncthreads();
+
+  for (int z = z0; z < z1; ++z) {
+    float pre[2];
+    const int pz = z + 2;
+    const bool prefetch = pz <= z1;
+    if (prefetch) load_plane_regs(g, pz, x0, y0, G, pre);
+
+    if (inside) {
+      const int i = x + G.nx * (y + G.ny * z);
+      float v[kSlots];
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {  // s is a compile-time constant here
+        const int b = slot_bits(s), sg1 = slot_sign(s);
+        v[s] = sg[(z + sg1 * (b >> 2)) & 3][c + sg1 * ((b & 1) + ((b >> 1) & 1) * SX)];
+      }
+      const float hc = sg[z & 3][c];
+      const Star st = eval_values(v, hc);
+      const uint32_t r = __ldcs(&ref[i]);
+      // targets as a 15-bit mask over the closed star (bit 14 = self)
+      uint32_t tgt = 0;
+      // R1: the g-largest neighbour is an impostor -> decrease it
+      if (st.up != ref_up(r)) { tgt |= 1u << st.up; n1 += 1; }
+      // R2: the g-smallest neighbour changed -> decrease the true N_min
+      if (st.dn != ref_dn(r)) { tgt |= 1u << ref_dn(r); n2 += 1; }
+      // R3 (amb-7, amb-8): flipped pairs at f-saddles and at
+      // vertices whose type (nlc, nuc) changed; target = the f-smaller end
+      const uint32_t flow = ref_flow(r);
+      const uint32_t flip = st.lower ^ flow;
+      if (flip) {
+        bool apply = ref_saddle(r);
+        if (!apply) {
+          int nl, nu;
+          link_type(st.lower, valid_mask(x, y, z, G), nl, nu);
+          apply = (nl != ref_nlc(r)) || (nu != ref_nuc(r));
+        }
+        if (apply) {
+          n3 += __popc(flip);
+          tgt |= flip & flow;
+          if (flip & ~flow) tgt |= 1u << kSelf;
+        }
+      }
+      for (; tgt; tgt &= tgt - 1) {
+        const int s = __ffs(tgt) - 1;
+        if (s == kSelf) {
+          sm[z & 3][c] = 1;
+        } else {
+          const int b = slot_bits(s), sg1 = slot_sign(s);
+          sm[(z + sg1 * (b >> 2)) & 3][c + sg1 * ((b & 1) + ((b >> 1) & 1) * SX)] = 1;
+        }
+      }
+      if (slots) slots[i] = (uint8_t)(st.dn | (st.up << 4));
+    }
+    if (prefetch) store_plane_regs(sg[pz & 3], pre);
+    for (int k = tid; k < SP; k += NT) sm[pz & 3][k] = 0;  // buffer of plane z-2 (flushed)
+    __syncthreads();
+    if (z - 1 >= z0) flush_plane(marks, sm[(z - 1) & 3], z - 1, x0, y0, true, G);
+    else if (z - 1 >= 0) flush_plane(marks, sm[(z - 1) & 3], z - 1, x0, y0, false, G);
+    __syncthreads();
+  }
+  // epilogue: the last interior plane and the halo plane above the chunk
+  if (z1 - 1 >= z0) flush_plane(marks, sm[(z1 - 1) & 3], z1 - 1, x0, y0, true, G);
+  if (z1 < G.nz) flush_plane(marks, sm[z1 & 3], z1, x0, y0, false, G);
+
   warp_add(&cnt[C_N1 + 0], n1);
   warp_add(&cnt[C_N1 + 1], n2);
   warp_add(&cnt[C_N1 + 2], n3);
@@ -309,90 +421,184 @@ __global__ void __launch_bounds__(128) k_stencil(const float *__restrict__ g,
 // R4 (C2): adjacent saddles a = S[k] <_f b = S[k+1]; if b <_g a,
 // decrease a (the f-smaller).
 __global__ void k_saddle_order(const float *__restrict__ g, const int32_t *__restrict__ S,
-                               int nS, uint8_t *mark, unsigned long long *cnt) {
+                               int nS, uint32_t *marks, GridP G, unsigned long long *cnt) {
   unsigned n4 = 0;
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k + 1 < nS) {
     int a = S[k], b = S[k + 1];
     if (sos_less_g(g, b, a)) {
-      mark[a] = 1;
+      mark_vertex(marks, a, G);
       n4 = 1;
     }
   }
   warp_add(&cnt[C_N1 + 3], n4);
 }
 
-// R5 / R6 (C3): for a join saddle s, m2 = <_g-largest minimum
-// reached from the g-lower link; if m2 != m1(s) decrease m2.  For a split
-// saddle, M2 = <_g-smallest maximum from the g-upper link; if M2 != M1(s)
-// decrease M1(s) (amb-12).
-__global__ void k_events(const float *__restrict__ g, const int32_t *__restrict__ sl, int n,
-                         const int32_t *__restrict__ lab, const int32_t *__restrict__ ref_ext,
-                         int split, uint8_t *mark, GridP G, unsigned long long *cnt) {
-  unsigned hit = 0;
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) {
-    int s = sl[k];
-    int x = s % G.nx, y = (s / G.nx) % G.ny, z = s / (G.nx * G.ny);
-    uint32_t valid = valid_mask(x, y, z, G);
-    float gs = g[s];
-    int best = -1;
-    float bv = 0.0f;
-#pragma unroll
-    for (int slot = 0; slot < kSlots; ++slot) {
-      if (!(valid & (1u << slot))) continue;
-      int u = s + G.delta[slot];
-      float gu = g[u];
-      bool lower = (slot < 7) ? (gu <= gs) : (gu < gs);
-      if (lower == (bool)split) continue;
-      int e = lab[u];
-      float ge = g[e];
-      bool take;
-      if (best < 0) take = true;
-      else if (!split) take = (bv < ge) || (bv == ge && best < e);  // max
-      else take = (ge < bv) || (ge == bv && e < best);               // min
-      if (take) { best = e; bv = ge; }
-    }
-    int want = ref_ext[k];
-    if (best >= 0 && best != want) {
-      mark[split ? want : best] = 1;
-      hit = 1;
+// Terminus of the steepest path from u (O6): follow 4-bit slot pointers.
+// FROM_REF: pointers of f (ref word bits 14-17 / 18-21); else of g (slot
+// bytes written by the stencil, low / high nibble).
+template <bool UP, bool FROM_REF>
+__device__ __forceinline__ int walk(int u, const uint8_t *__restrict__ slots,
+                                    const uint32_t *__restrict__ ref, const GridP &G) {
+  int w = u;
+  for (;;) {
+    int s;
+    if (FROM_REF) s = (__ldg(&ref[w]) >> (UP ? 18 : 14)) & 15;
+    else s = (__ldg(&slots[w]) >> (UP ? 4 : 0)) & 15;
+    if (s == kSelf) return w;
+    const int b = slot_bits(s);
+    const int d = (b & 1) + ((b >> 1) & 1) * G.nx + (b >> 2) * G.nx * G.ny;
+    w += slot_sign(s) * d;
+  }
+}
+
+// R5 / R6 (C3): for a join saddle s, m2 = <_h-largest minimum
+// reached from the h-lower link; for a split saddle, M2 = <_h-smallest
+// maximum from the h-upper link.  16 lanes per saddle, one per slot, each
+// walking its own integral path; a 16-lane shuffle reduction picks the
+// extremum.  FROM_REF: h = f, the result is m1 / M1 (reference).
+// Else h = g: if the pick differs from m1 (M1), mark m2 (join) or
+// M1 (split, amb-12).
+template <bool SPLIT, bool FROM_REF>
+__global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
+                                                const int32_t *__restrict__ sl, int n,
+                                                const uint8_t *__restrict__ slots,
+                                                const uint32_t *__restrict__ ref,
+                                                int32_t *ref_ext, uint32_t *marks, GridP G,
+                                                unsigned long long *cnt) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = gt >> 4, l16 = threadIdx.x & 15;
+  const bool active = k < n;
+  int best = -1;
+  float bv = 0.0f;
+  int s = 0;
+  if (active) {
+    s = __ldg(&sl[k]);
+    if (l16 < kSlots) {
+      int x = s % G.nx, yz = s / G.nx, y = yz % G.ny, z = yz / G.ny;
+      uint32_t valid = valid_mask(x, y, z, G);
+      if (valid & (1u << l16)) {
+        int u = s + G.delta[l16];
+        float hs = h[s], hu = h[u];
+        bool lower = (l16 < 7) ? (hu <= hs) : (hu < hs);
+        if (lower != SPLIT) {
+          best = walk<SPLIT, FROM_REF>(u, slots, ref, G);
+          bv = h[best];
+        }
+      }
     }
   }
-  warp_add(&cnt[C_N1 + 4 + split], hit);
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) {
+    int ob = __shfl_xor_sync(0xffffffffu, best, off);
+    float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+    bool take;
+    if (ob < 0) take = false;
+    else if (best < 0) take = true;
+    else if (!SPLIT) take = (bv < ov) || (bv == ov && best < ob);  // SoS max
+    else take = (ov < bv) || (ov == bv && ob < best);               // SoS min
+    if (take) { best = ob; bv = ov; }
+  }
+  unsigned hit = 0;
+  if (active && l16 == 0) {
+    if (FROM_REF) {
+      ref_ext[k] = best;
+    } else {
+      int want = ref_ext[k];
+      if (best >= 0 && best != want) {
+        mark_vertex(marks, SPLIT ? want : best, G);
+        hit = 1;
+      }
+    }
+  }
+  if (!FROM_REF) warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
 }
 
 // ---------------------------------------------------- count + edit (O9)
-// V_t = #marked; for each marked i not at lo = RU(f_i - xi): a step of
-// Delta (clamped at lo) while c_i < N, else the lossless clamp; c_i++.
-// Marks are cleared for the next round.
-__global__ void k_count_edit(float *g, uint8_t *c, uint8_t *mark, const float *__restrict__ f,
-                             int64_t V, float xi, float delta, int N, int do_edit,
-                             unsigned long long *cnt) {
+// Warp-per-word: lanes of a warp cover the 32 vertices of one mark word (one
+// row segment), a persistent grid strides over the words, 4 words in flight
+// per warp.  V_t = popcount of the words; for each marked i not at
+// lo = RU(f_i - xi): a step of Delta (clamped at lo) while c_i < N, else the
+// lossless clamp; c_i++.  Words are cleared for the next round.
+__device__ __forceinline__ void edit_vertex(float *__restrict__ g, uint8_t *__restrict__ c,
+                                            const float *__restrict__ f, size_t i, float xi,
+                                            float delta, int N, unsigned &ap) {
+  float lo = __fsub_ru(f[i], xi);
+  float gi = g[i];
+  if (gi == lo) return;
+  int ci = c[i];
+  float t;
+  if (ci < N) {
+    t = __fsub_rn(gi, delta);
+    t = (t < lo) ? lo : t;
+  } else {
+    t = lo;
+  }
+  g[i] = t;
+  c[i] = (uint8_t)(ci + 1);
+  ++ap;
+}
+
+__global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
+                                                    uint8_t *__restrict__ c,
+                                                    uint32_t *__restrict__ marks,
+                                                    const float *__restrict__ f, GridP G,
+                                                    float xi, float delta, int N, int do_edit,
+                                                    unsigned long long *cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwords = (int64_t)G.ny * G.nz * G.W;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned vt = 0, ap = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (!mark[i]) continue;
-    ++vt;
-    mark[i] = 0;
-    if (!do_edit) continue;
-    float lo = __fsub_ru(f[i], xi);
-    float gi = g[i];
-    if (gi == lo) continue;
-    int ci = c[i];
-    float t;
-    if (ci < N) {
-      t = __fsub_rn(gi, delta);
-      t = (t < lo) ? lo : t;
-    } else {
-      t = lo;
+  for (int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4; w0 < nwords;
+       w0 += nwarps * 4) {
+    // lanes 0..3 fetch the 4 words of this batch; broadcast by shuffle
+    uint32_t mine = (lane < 4 && w0 + lane < nwords) ? marks[w0 + lane] : 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t word = __shfl_sync(0xffffffffu, mine, j);
+      if (!word) continue;
+      const int64_t w = w0 + j;
+      if (lane == 0) {
+        vt += __popc(word);
+        marks[w] = 0u;
+      }
+      if (do_edit && ((word >> lane) & 1u)) {
+        const int64_t row = w / G.W;
+        const int x = (int)(w - row * G.W) * 32 + lane;
+        edit_vertex(g, c, f, (size_t)x + (size_t)G.nx * row, xi, delta, N, ap);
+      }
     }
-    g[i] = t;
-    c[i] = (uint8_t)(ci + 1);
-    ++ap;
   }
   warp_add(&cnt[C_VT], vt);
   warp_add(&cnt[C_APPLIED], ap);
+}
+
+// ------------------------------------------ full labels (outputs only, O6)
+__global__ void k_slots_to_ptrs(const uint8_t *__restrict__ slots, int32_t *pdn, int32_t *pup,
+                                GridP G) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= G.V) return;
+  uint8_t s = slots[i];
+  pdn[i] = slot_target((int)i, s & 15, G);
+  pup[i] = slot_target((int)i, s >> 4, G);
+}
+
+// lab[] holds, for every vertex, a pointer to an ancestor in its steepest
+// forest; a round replaces it by its pointer's pointer.  Reads may see
+// pointers other threads already advanced (still ancestors), which only
+// speeds convergence; the fixpoint (roots) is unique.
+__global__ void k_jump(int32_t *lab, int64_t V, unsigned long long *cnt) {
+  unsigned changed = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int w = lab[i];
+    int w2 = lab[w];
+    if (w2 != w) {
+      lab[i] = w2;
+      changed = 1;
+    }
+  }
+  if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) atomicOr(&cnt[C_CHANGED], 1ull);
 }
 
 // ------------------------------------------------------- min / max of f
