@@ -4,14 +4,14 @@
 One *step* = one full correction (exactz_correct: validate, reference of f,
 every detect/edit round until no violation remains) of config C2 — the
 512^3 float32 Nyx-like field at relative eps 1e-3 (BASELINE.json configs[1]) —
-with inputs resident in HBM.  value = 4 * V * n_ranks / (max-over-ranks step
-time), decimal GB/s of field processed (the paper's OT).
+with inputs resident in HBM.  value = 4 * V / (max-over-ranks step time),
+decimal GB/s of field processed (the paper's OT).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
   python bench.py --impl reference ...   # the CPU oracle arm
 
-N > 1 (torchrun, one rank per GPU): every rank corrects its own replica of the
-workload (scaling "weak"; the sharded z-slab path is reported separately).
+N > 1 (torchrun, one rank per GPU): the z-slab path (exactz_correct_sharded)
+corrects the same field split over the ranks (scaling "strong").
 Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
@@ -215,12 +215,30 @@ def main():
 
     f, g, xi = S.make(args.config, device=dev)
     V = f.numel()
-    out = torch.empty_like(g)
+    wname = workload_name(args.config, f)
     stream = torch.cuda.current_stream()
+    sharded = ws > 1
+    if sharded:
+        # strong scaling: the z-slabs of ONE field over the ranks (NCCL inside)
+        from paper_2604_01397_b200 import dist as D
+        comm = D.open_comm(local)
+        z0, zc = D.slab_of(f.shape[0], ws, rank)
+        dims = (f.shape[2], f.shape[1], f.shape[0])
+        f_run, g_run = f[z0:z0 + zc].contiguous(), g[z0:z0 + zc].contiguous()
+        del f, g
+        torch.cuda.empty_cache()
+        out = torch.empty_like(g_run)
 
-    def step(profile=False):
-        return E.exactz_correct(f, g, xi, out=out, flags=E.PROFILE if profile else 0,
-                                stats_cap=100000)
+        def step(profile=False):
+            return E.exactz_correct_sharded(comm, f_run, g_run, dims, xi, out=out,
+                                            stats_cap=100000)
+    else:
+        f_run, g_run = f, g
+        out = torch.empty_like(g)
+
+        def step(profile=False):
+            return E.exactz_correct(f, g, xi, out=out, flags=E.PROFILE if profile else 0,
+                                    stats_cap=100000)
 
     for _ in range(args.warmup):
         r0 = step()
@@ -247,11 +265,12 @@ def main():
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
-    value = 4.0 * V * ws / (ms_step / 1e3) / 1e9
+    value = 4.0 * V / (ms_step / 1e3) / 1e9  # the whole field (strong scaling for N > 1)
 
     r = results[-1]
     iters = r.iters
-    # roofline of the dominant kernel class (CUDA events on the launch stream)
+    # roofline of the dominant kernel class (CUDA events on the launch stream;
+    # single-GPU call only: the sharded call does not profile per kernel)
     agg = {}
     for res in results:
         for k, (ms, n, b) in res.kernels.items():
@@ -259,8 +278,8 @@ def main():
             a[0] += ms
             a[1] += n
             a[2] += b
-    dom = max(agg, key=lambda k: agg[k][0])
-    dms, dn, dbytes = agg[dom]
+    dom = max(agg, key=lambda k: agg[k][0]) if agg else "stencil"
+    dms, dn, dbytes = agg.get(dom, (0.0, 0, 0))
     peak, peak_src = peaks()
     achieved = (dbytes / dn) / ((dms / dn) / 1e3) / 1e9 if dn and dms else None
     share = dms / (ms_step * args.steps)
@@ -281,10 +300,20 @@ def main():
     except Exception:
         pass
 
-    # ---------------- e2e: the C-ABI call with HOST buffers (pinned)
-    fh, gh = f.cpu().pin_memory(), g.cpu().pin_memory()
+    # ---------------- e2e: host buffers in, host result out, every step
+    fh, gh = f_run.cpu().pin_memory(), g_run.cpu().pin_memory()
     oh = torch.empty_like(gh).pin_memory()
-    E.exactz_correct_host(fh, gh, xi, out=oh)  # warm
+
+    def e2e_step():
+        if sharded:  # H2D of this rank's slab, the sharded call, D2H of its result
+            fd = fh.to(dev, non_blocking=True)
+            gd = gh.to(dev, non_blocking=True)
+            rr = E.exactz_correct_sharded(comm, fd, gd, dims, xi, out=out)
+            oh.copy_(out, non_blocking=True)
+            return rr
+        return E.exactz_correct_host(fh, gh, xi, out=oh)  # copies inside the C call
+
+    e2e_step()  # warm
     ke = max(1, min(args.steps, 3))
     if ws > 1:
         dist.barrier()
@@ -292,7 +321,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(ke):
-        E.exactz_correct_host(fh, gh, xi, out=oh)
+        e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
     te = torch.tensor([e0.elapsed_time(e1) / ke], dtype=torch.float64, device=dev)
@@ -304,7 +333,7 @@ def main():
     # ---------------- CPU baseline: the oracle on a bounded crop (rank 0, N = 1)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        fs, gs = crop(f, g, args.cpu_sample)
+        fs, gs = crop(f_run, g_run, args.cpu_sample)
         dt, ro = oracle_run(fs.cpu(), gs.cpu(), xi)
         cpu = {"value": 4 * fs.numel() / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
                "sample": (f"centred {'x'.join(str(d) for d in reversed(tuple(fs.shape)))} crop "
@@ -316,20 +345,23 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_name(args.config, f), "V": V, "xi": xi,
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wname, "V": V, "xi": xi,
                        "iterations": iters, "status": r.status,
                        "ms_setup": r.ms_setup, "ms_loop": r.ms_loop,
                        "l2": f"inputs {4 * V / 1e6:.0f} MB per field > 126 MB L2 (no flush)",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "parallelism": (f"z-slabs x{ws} (NCCL send/recv + all-gather + "
+                                       "all-reduce)") if sharded else "single GPU",
                        "edit_pct": None},
             "iterations": iters,
             "hbm_frac": roofline["frac"],
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "e2e": {"value": 4.0 * V * ws / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
+            "e2e": {"value": 4.0 * V / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * V, "d2h_bytes_per_step": 4 * V,
+                    "path": "torch H2D + exactz_correct_sharded + D2H per rank" if sharded
+                    else "exactz_correct_host (pinned host buffers, copies inside the C call)",
                     "ms_per_step": e2e_ms, "bit_equal_to_device_run": same},
             "gpu_launches": launches,
             "clocks": ck,
@@ -337,6 +369,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
+        comm.close()
         dist.destroy_process_group()
     return 0
 

@@ -136,18 +136,34 @@ exactz_status exactz_eps_from_relative(const float *f, int64_t n, double rel, fl
  * every rank calls with identical scalars.  `id` is 128 bytes from
  * exactz_nccl_unique_id on rank 0, broadcast by the caller. */
 typedef struct exactz_comm exactz_comm;
+/* The z-slab of `rank` in an nz-plane field over `nranks` ranks: planes
+ * [*z_begin, *z_begin + *z_count); the first nz % nranks ranks get one extra. */
+exactz_status exactz_slab_range(int64_t nz, int nranks, int rank, int64_t *z_begin,
+                                int64_t *z_count);
 exactz_status exactz_nccl_unique_id(uint8_t id[128]);
 exactz_status exactz_comm_init(const uint8_t id[128], int nranks, int rank, int cuda_device,
                                exactz_comm **out);
 exactz_status exactz_comm_destroy(exactz_comm *comm);
 /* f_local / g_local / out_local: the z_count planes [z_begin, z_begin+z_count)
- * of the global field (global_dims = {nx, ny, nz}).  out_local is bit-equal to
+ * of the global field (global_dims = {nx, ny, nz}); rank r must own exactly
+ * the planes of the split "the first nz % nranks ranks get one extra plane"
+ * (else EXACTZ_EINVAL).  label_min/max are not supported (EXACTZ_EUNSUPPORTED);
+ * edit_counts covers the local planes.  out_local is bit-equal to
  * the same planes of the single-GPU out; *iters identical on every rank. */
 exactz_status exactz_correct_sharded(exactz_comm *comm, const float *f_local,
                                      const float *g_local, const int64_t global_dims[3],
                                      int64_t z_begin, int64_t z_count, float eps_abs,
                                      float *out_local, uint32_t *iters, const exactz_opts *opts,
                                      void *stream);
+
+/* Single-process slab decomposition: runs the sharded algorithm with
+ * `nslabs` virtual ranks on the current device (loopback transport instead of
+ * NCCL); f, g_in, out are whole-field device buffers.  Validates the sharded
+ * path on one GPU: out is bit-equal to exactz_correct's.  label_min/max are
+ * not supported (EXACTZ_EUNSUPPORTED). */
+exactz_status exactz_correct_slabs(const float *f, const float *g_in, const int64_t dims[3],
+                                   float eps_abs, int nslabs, float *out, uint32_t *iters,
+                                   const exactz_opts *opts, void *stream);
 
 const char *exactz_strerror(exactz_status s);
 const char *exactz_last_error(void);

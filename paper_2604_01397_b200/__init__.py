@@ -68,6 +68,12 @@ _lib.exactz_comm_destroy.restype = C.c_int
 _lib.exactz_correct_sharded.argtypes = [_P, _P, _P, _i64p, C.c_int64, C.c_int64, C.c_float, _P,
                                         C.POINTER(C.c_uint32), C.POINTER(Opts), _P]
 _lib.exactz_correct_sharded.restype = C.c_int
+_lib.exactz_correct_slabs.argtypes = [_P, _P, _i64p, C.c_float, C.c_int, _P,
+                                      C.POINTER(C.c_uint32), C.POINTER(Opts), _P]
+_lib.exactz_correct_slabs.restype = C.c_int
+_lib.exactz_slab_range.argtypes = [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int64)]
+_lib.exactz_slab_range.restype = C.c_int
 
 
 def lib() -> C.CDLL:
@@ -214,3 +220,79 @@ def status_of(fn, *a, **kw) -> int:
         return r.status if isinstance(r, CorrectResult) else OK
     except ExactzError as e:
         return e.status
+
+
+# ----------------------------------------------------------------- sharded path
+def exactz_slab_range(nz: int, nranks: int, rank: int):
+    """(z_begin, z_count) of rank's z-slab (the C ABI's split)."""
+    a, b = C.c_int64(0), C.c_int64(0)
+    s = _lib.exactz_slab_range(nz, nranks, rank, C.byref(a), C.byref(b))
+    if s != OK:
+        raise ExactzError(s, "exactz_slab_range")
+    return a.value, b.value
+
+
+def exactz_correct_slabs(f, g_in, eps: float, nslabs: int, out=None, *, N: int = 5,
+                         max_iters: int = 0, flags: int = 0, edit_counts=None,
+                         stats_cap: int = 0, stream=None) -> CorrectResult:
+    """The sharded algorithm with `nslabs` virtual ranks on the current GPU
+    (loopback transport): bit-equal to exactz_correct."""
+    import torch
+    if out is None:
+        out = torch.empty_like(g_in)
+    o, st, rows = _opts(N, max_iters, flags, edit_counts, None, None, stats_cap)
+    iters = C.c_uint32(0)
+    s = _lib.exactz_correct_slabs(_ptr(f), _ptr(g_in), _dims(f), float(eps), nslabs, _ptr(out),
+                                  C.byref(iters), C.byref(o), _stream(stream))
+    if s not in (OK, ESTUCK):
+        raise ExactzError(s, "exactz_correct_slabs")
+    res = _result(s, iters, st, rows)
+    res.out = out
+    return res
+
+
+def exactz_nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    s = _lib.exactz_nccl_unique_id(buf)
+    if s != OK:
+        raise ExactzError(s, "exactz_nccl_unique_id")
+    return bytes(buf)
+
+
+class Comm:
+    """An NCCL communicator of the sharded path (one rank per GPU)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        self.h = C.c_void_p(0)
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        s = _lib.exactz_comm_init(buf, nranks, rank, device, C.byref(self.h))
+        if s != OK:
+            raise ExactzError(s, "exactz_comm_init")
+        self.nranks, self.rank = nranks, rank
+
+    def close(self):
+        if self.h:
+            _lib.exactz_comm_destroy(self.h)
+            self.h = C.c_void_p(0)
+
+
+def exactz_correct_sharded(comm: Comm, f_local, g_local, global_dims, eps: float, out=None, *,
+                           N: int = 5, max_iters: int = 0, flags: int = 0, edit_counts=None,
+                           stats_cap: int = 0, stream=None) -> CorrectResult:
+    """One rank of the z-slab decomposition: f_local/g_local are this rank's
+    planes (shape (z_count, ny, nx)); collective over comm."""
+    import torch
+    if out is None:
+        out = torch.empty_like(g_local)
+    z0, zc = exactz_slab_range(int(global_dims[2]), comm.nranks, comm.rank)
+    o, st, rows = _opts(N, max_iters, flags, edit_counts, None, None, stats_cap)
+    iters = C.c_uint32(0)
+    dims = (C.c_int64 * 3)(*[int(x) for x in global_dims])
+    s = _lib.exactz_correct_sharded(comm.h, _ptr(f_local), _ptr(g_local), dims, z0, zc,
+                                    float(eps), _ptr(out), C.byref(iters), C.byref(o),
+                                    _stream(stream))
+    if s not in (OK, ESTUCK):
+        raise ExactzError(s, "exactz_correct_sharded")
+    res = _result(s, iters, st, rows)
+    res.out = out
+    return res

@@ -11,14 +11,14 @@ LIB = os.path.join(PKG, "libexactz.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["exactz.cu"]
-HEADERS = ["kernels.cuh", "mesh.cuh"]
+HEADERS = ["kernels.cuh", "mesh.cuh", "sharded.cuh"]
 
 FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
     # IEEE-exact float semantics: the path must be bit-exact with the oracle
     "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-Xcompiler", "-Wno-deprecated-declarations",
     "-shared",
 ]
 
@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *FLAGS, f"-DEXACTZ_GIT=\"{_git()}\"", "-I", os.path.join(ROOT, "include"),
-           "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
+           "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES], "-lnccl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

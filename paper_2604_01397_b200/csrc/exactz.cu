@@ -160,6 +160,10 @@ struct Ctx {
     G.W = (G.nx + 31) / 32;
     for (int s = 0; s < kSlots; ++s)
       G.delta[s] = kOff[s][0] + G.nx * (kOff[s][1] + G.ny * kOff[s][2]);
+    G.zoff = 0;
+    G.gnz = G.nz;
+    G.zb = 0;
+    G.ze = G.nz;
     // z chunk per stencil CTA: enough CTAs to fill 148 SMs several times over,
     // few enough halo planes (2 per chunk) to keep re-reads small
     int64_t cols = (int64_t)((G.nx + TX - 1) / TX) * ((G.ny + TY - 1) / TY);
@@ -184,7 +188,7 @@ struct Ctx {
   // Keep freed stream-ordered memory in the device's default pool between
   // calls (the default release threshold 0 returns it to the OS at every
   // sync, making each call re-map its scratch).
-  static void keep_pool() {
+  static void keep_pool() {  // also used by the sharded path
     int dev = 0;
     CK(cudaGetDevice(&dev));
     cudaMemPool_t pool;
@@ -196,14 +200,10 @@ struct Ctx {
     static thread_local uint8_t lut[1 << kSlots];
     static thread_local bool ready = false;
     if (!ready) {
-      for (uint32_t m = 0; m < (1u << kSlots); ++m) {
-        int nl = link_components_t(m, kLink.adj);
-        int nu = link_components_t(0x3FFFu & ~m, kLink.adj);
-        lut[m] = (uint8_t)(nl | (nu << 4));
-      }
+      for (uint32_t m = 0; m < (1u << kSlots); ++m) lut[m] = (uint8_t)link_components_t(m, kLink.adj);
       ready = true;
     }
-    CK(cudaMemcpyToSymbolAsync(d_lut, lut, sizeof(lut), 0, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyToSymbolAsync(d_comp, lut, sizeof(lut), 0, cudaMemcpyHostToDevice, s));
   }
   size_t mark_words() const { return (size_t)G.ny * G.nz * G.W; }
   void zero() { CK(cudaMemsetAsync(cnt, 0, C_NCOUNTERS * sizeof(unsigned long long), s)); }
@@ -267,7 +267,7 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
   // reached extrema's values and ids
   C.run(FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS, 128ull * n, true, [&] {
     k_events<SPLIT, FROM_REF><<<(unsigned)((threads + 255) / 256), 256, 0, C.s>>>(
-        h, sl, n, slots, ref, ext, marks, C.G, C.cnt);
+        h, sl, n, slots, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt);
   });
 }
 
@@ -461,6 +461,8 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
 
 }  // namespace exz
 
+#include "sharded.cuh"
+
 using namespace exz;
 
 template <class Fn>
@@ -578,29 +580,101 @@ exactz_status exactz_eps_from_relative(const float *f, int64_t n, double rel, fl
   });
 }
 
-exactz_status exactz_nccl_unique_id(uint8_t id[128]) {
-  (void)id;
-  set_err("exactz_nccl_unique_id", "sharded path not built");
-  return EXACTZ_EUNSUPPORTED;
+exactz_status exactz_slab_range(int64_t nz, int nranks, int rank, int64_t *z_begin,
+                                int64_t *z_count) {
+  if (nz < 1 || nranks < 1 || rank < 0 || rank >= nranks || !z_begin || !z_count)
+    return EXACTZ_EINVAL;
+  slab_range(nz, nranks, rank, z_begin, z_count);
+  return EXACTZ_OK;
 }
+
+exactz_status exactz_nccl_unique_id(uint8_t id[128]) {
+  return guarded([&]() -> exactz_status {
+    if (!id) return EXACTZ_EINVAL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId u;
+    NK(ncclGetUniqueId(&u));
+    std::memcpy(id, &u, 128);
+    return EXACTZ_OK;
+  });
+}
+
 exactz_status exactz_comm_init(const uint8_t id[128], int nranks, int rank, int cuda_device,
                                exactz_comm **out) {
-  (void)id; (void)nranks; (void)rank; (void)cuda_device; (void)out;
-  set_err("exactz_comm_init", "sharded path not built");
-  return EXACTZ_EUNSUPPORTED;
+  return guarded([&]() -> exactz_status {
+    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return EXACTZ_EINVAL;
+    CK(cudaSetDevice(cuda_device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    exactz_comm *c = new exactz_comm{nullptr, nranks, rank, cuda_device};
+    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+    if (r != ncclSuccess) {
+      set_err("ncclCommInitRank", ncclGetErrorString(r));
+      delete c;
+      return EXACTZ_ENCCL;
+    }
+    *out = c;
+    return EXACTZ_OK;
+  });
 }
+
 exactz_status exactz_comm_destroy(exactz_comm *comm) {
-  (void)comm;
-  return EXACTZ_EUNSUPPORTED;
+  return guarded([&]() -> exactz_status {
+    if (!comm) return EXACTZ_EINVAL;
+    ncclResult_t r = ncclCommDestroy(comm->nccl);
+    delete comm;
+    if (r != ncclSuccess) {
+      set_err("ncclCommDestroy", ncclGetErrorString(r));
+      return EXACTZ_ENCCL;
+    }
+    return EXACTZ_OK;
+  });
 }
+
 exactz_status exactz_correct_sharded(exactz_comm *comm, const float *f_local, const float *g_local,
                                      const int64_t global_dims[3], int64_t z_begin,
                                      int64_t z_count, float eps_abs, float *out_local,
                                      uint32_t *iters, const exactz_opts *opts, void *stream) {
-  (void)comm; (void)f_local; (void)g_local; (void)global_dims; (void)z_begin; (void)z_count;
-  (void)eps_abs; (void)out_local; (void)iters; (void)opts; (void)stream;
-  set_err("exactz_correct_sharded", "sharded path not built");
-  return EXACTZ_EUNSUPPORTED;
+  return guarded([&]() -> exactz_status {
+    if (!comm || !f_local || !g_local || !out_local || !global_dims) return EXACTZ_EINVAL;
+    int64_t z0 = 0, cnt = 0;
+    slab_range(global_dims[2], comm->nranks, comm->rank, &z0, &cnt);
+    if (z_begin != z0 || z_count != cnt) {
+      set_err("exactz_correct_sharded", "slab does not match slab_range(nz, nranks, rank)");
+      return EXACTZ_EINVAL;
+    }
+    NcclTransport T(comm, (cudaStream_t)stream);
+    return sharded_impl(T, {f_local}, {g_local}, {out_local},
+                        {opts ? opts->edit_counts : nullptr}, global_dims, eps_abs, iters, opts,
+                        (cudaStream_t)stream);
+  });
+}
+
+exactz_status exactz_correct_slabs(const float *f, const float *g_in, const int64_t dims[3],
+                                   float eps_abs, int nslabs, float *out, uint32_t *iters,
+                                   const exactz_opts *opts, void *stream) {
+  return guarded([&]() -> exactz_status {
+    int64_t V = 0;
+    if (!f || !g_in || !out || nslabs < 1 || check_dims(dims, &V) != EXACTZ_OK)
+      return EXACTZ_EINVAL;
+    if (dims[2] < nslabs) return EXACTZ_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena A(s);
+    LoopTransport T(nslabs, s, A);
+    std::vector<const float *> fi, gi;
+    std::vector<float *> o;
+    std::vector<uint8_t *> co;
+    const size_t P = (size_t)dims[0] * dims[1];
+    for (int r = 0; r < nslabs; ++r) {
+      int64_t z0 = 0, cnt = 0;
+      slab_range(dims[2], nslabs, r, &z0, &cnt);
+      fi.push_back(f + z0 * P);
+      gi.push_back(g_in + z0 * P);
+      o.push_back(out + z0 * P);
+      co.push_back(opts && opts->edit_counts ? opts->edit_counts + z0 * P : nullptr);
+    }
+    return sharded_impl(T, fi, gi, o, co, dims, eps_abs, iters, opts, s);
+  });
 }
 
 const char *exactz_strerror(exactz_status s) {

@@ -24,8 +24,11 @@ __constant__ LinkTables c_link = kLink;
 __host__ __device__ __forceinline__ int slot_bits(int s) { return s >= 7 ? s - 6 : 7 - s; }
 __host__ __device__ __forceinline__ int slot_sign(int s) { return s >= 7 ? 1 : -1; }
 
-// (nlc | nuc << 4) of every interior lower mask (slot order), built on the host
-__device__ uint8_t d_lut[1 << kSlots];
+// Number of connected components of the link graph induced on any subset M of
+// the 14 slots (O4), built on the host from the Kuhn tables.  The induced
+// subgraph on M does not depend on the other slots, so a clipped (boundary)
+// link is handled by the same table: nlc = comp[lower], nuc = comp[valid & ~lower].
+__device__ uint8_t d_comp[1 << kSlots];
 
 enum Counter {
   C_VT = 0,       // distinct marked vertices
@@ -37,13 +40,20 @@ enum Counter {
   C_NSADDLE = 11,
   C_KEYMIN = 12,  // eps_from_relative: ordered-key min / max
   C_KEYMAX = 13,
+  C_NREMOTE = 14,  // sharded: remote marks appended by k_events
   C_NCOUNTERS = 16
 };
 
+// Geometry of the (local) grid a kernel works on.  Single GPU: the whole
+// field (zoff = 0, gnz = nz, owned planes [zb, ze) = [0, nz)).  Sharded: one
+// z-slab with a ghost plane on each side (local plane 0 is global plane
+// zoff), owned planes [1, nz-1).
 struct GridP {
-  int nx, ny, nz, V;
+  int nx, ny, nz, V;  // local extent (V = nx*ny*nz)
   int W;              // 32-bit words per row of the mark bitmap, ceil(nx/32)
   int delta[kSlots];  // linear offset of each slot
+  int zoff, gnz;      // global z of local plane 0, global nz
+  int zb, ze;         // owned local planes [zb, ze)
 };
 
 // ref word layout (one uint32 per vertex, computed once from f):
@@ -61,20 +71,21 @@ __host__ __device__ constexpr bool ref_saddle(uint32_t r) { return (r >> 28) & 1
 __host__ __device__ constexpr bool ref_join(uint32_t r) { return (r >> 29) & 1; }
 __host__ __device__ constexpr bool ref_split(uint32_t r) { return (r >> 30) & 1; }
 
+// slots of vertex (x, y, local z) whose neighbour exists in the global domain
 __device__ __forceinline__ uint32_t valid_mask(int x, int y, int z, const GridP &G) {
   uint32_t m = 0x3FFFu;
+  const int zg = z + G.zoff;
   if (x == 0) m &= ~(uint32_t)c_link.req[0];
   if (x == G.nx - 1) m &= ~(uint32_t)c_link.req[1];
   if (y == 0) m &= ~(uint32_t)c_link.req[2];
   if (y == G.ny - 1) m &= ~(uint32_t)c_link.req[3];
-  if (z == 0) m &= ~(uint32_t)c_link.req[4];
-  if (z == G.nz - 1) m &= ~(uint32_t)c_link.req[5];
+  if (zg == 0) m &= ~(uint32_t)c_link.req[4];
+  if (zg == G.gnz - 1) m &= ~(uint32_t)c_link.req[5];
   return m;
 }
 
 // Number of connected components of the link graph induced on `set`
-// (bit-parallel flood fill; O4).  Used for boundary vertices and to build the
-// interior LUT.
+// (bit-parallel flood fill; O4).  Used on the host to build d_comp.
 __host__ __device__ __forceinline__ uint32_t link_expand(uint32_t r, const uint16_t *adj) {
   uint32_t n = r;
 #pragma unroll
@@ -96,20 +107,11 @@ __host__ __device__ inline int link_components_t(uint32_t set, const uint16_t *a
   }
   return n;
 }
-__device__ __noinline__ int link_components(uint32_t set) {
-  return link_components_t(set, c_link.adj);
-}
 
 // (nlc, nuc) of a vertex with lower mask `lower` and valid mask `valid`.
 __device__ __forceinline__ void link_type(uint32_t lower, uint32_t valid, int &nl, int &nu) {
-  if (valid == 0x3FFFu) {
-    uint32_t t = d_lut[lower];
-    nl = t & 15;
-    nu = t >> 4;
-  } else {
-    nl = link_components(lower);
-    nu = link_components(valid & ~lower);
-  }
+  nl = __ldg(&d_comp[lower]);
+  nu = __ldg(&d_comp[valid & ~lower]);
 }
 
 struct Star {
@@ -225,7 +227,8 @@ __device__ __forceinline__ void reference_vertex(const float *__restrict__ f, co
            ((uint32_t)split << 30);
   if (sad) {
     unsigned long long k = atomicAdd(&cnt[C_NSADDLE], 1ull);
-    saddle_keys[k] = ((uint64_t)ordered_key(f[i]) << 32) | (uint32_t)i;
+    const uint32_t ig = (uint32_t)(i + G.zoff * G.nx * G.ny);  // global index (SoS)
+    saddle_keys[k] = ((uint64_t)ordered_key(f[i]) << 32) | ig;
   }
 }
 
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(128) k_reference(const float *__restrict__ f, 
                                                    uint32_t *__restrict__ ref,
                                                    uint64_t *saddle_keys,
                                                    unsigned long long *cnt) {
-  for (int row = blockIdx.y; row < G.ny * G.nz; row += gridDim.y)
+  for (int row = G.zb * G.ny + blockIdx.y; row < G.ze * G.ny; row += gridDim.y)
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < G.nx; x += gridDim.x * blockDim.x)
       reference_vertex(f, G, ref, saddle_keys, cnt, x, row % G.ny, row / G.ny);
 }
@@ -254,39 +257,50 @@ struct IsSplit {
 };
 
 // ------------------------------------------------------- detection (O8)
-// Stencil tile: 32 (x) x 8 (y) columns per CTA, marching along z through a
-// chunk of planes.  g planes z-1 .. z+2 live in a 4-deep shared-memory ring
-// with a 1-vertex halo; plane z+2 is prefetched into registers while plane z
-// is evaluated.  Marks are ORed into a shared ring of byte planes and flushed
-// to the global bitmap once complete: interior rows as one warp-ballot word,
-// halo cells as single-bit atomics.
+// Stencil tile: 32 (x) x 8 (y) columns per CTA (one warp per y row),
+// marching along z through a chunk of planes.  g planes z-1 .. z+2 live in a
+// 4-deep shared-memory ring with a 1-vertex halo; plane z+2 is prefetched
+// into registers while plane z is evaluated.
+// Marks: every vertex names its targets as a 15-bit mask over its closed
+// star; a warp turns the masks into one ballot per slot and ORs them, shifted
+// by the slot's x offset, into 64-bit shared rows (bit lx of row ly of a
+// plane buffer, lx = 0..33 covering x0-1 .. x0+32).  A plane is complete one
+// step after its last contributor and is flushed into the global bitmap with
+// at most 3 atomics per row (left halo bit, the 32 interior bits, right halo
+// bit).  One barrier per plane.
 constexpr int TX = 32, TY = 8, NT = TX * TY;
 constexpr int SX = TX + 2, SY = TY + 2, SP = SX * SY;  // 340 cells per plane
-constexpr int PERIM = 2 * SX + 2 * TY;                 // 84 halo cells per plane
 
-__device__ __forceinline__ void perim_cell(int t, int &ly, int &lx) {
-  if (t < SX) { ly = 0; lx = t; }
-  else if (t < 2 * SX) { ly = SY - 1; lx = t - SX; }
-  else if (t < 2 * SX + TY) { ly = 1 + (t - 2 * SX); lx = 0; }
-  else { ly = 1 + (t - 2 * SX - TY); lx = SX - 1; }
-}
-
-// Plane p of the tile with its halo into registers (2 cells per thread);
-// cells outside the domain (or a plane outside [0, nz)) read as NaN.
-__device__ __forceinline__ void load_plane_regs(const float *__restrict__ g, int p, int x0, int y0,
-                                                const GridP &G, float (&r)[2]) {
+// Per-thread offsets of its (up to 2) halo-tile cells within a plane, -1 when
+// outside the domain; computed once per CTA (V < 2^31: 32-bit offsets).
+struct PlaneCells {
+  int off[2];
+};
+__device__ __forceinline__ PlaneCells plane_cells(int x0, int y0, const GridP &G) {
   const int tid = threadIdx.y * TX + threadIdx.x;
+  PlaneCells pc;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     int c = tid + k * NT;
-    r[k] = __int_as_float(0x7fc00000);
-    if (c < SP && p >= 0 && p < G.nz) {
+    pc.off[k] = -1;
+    if (c < SP) {
       int ly = c / SX, lx = c - ly * SX;
       int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
-      if (gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny)
-        r[k] = g[gx + (size_t)G.nx * (gy + (size_t)G.ny * p)];
+      if (gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny) pc.off[k] = gx + G.nx * gy;
     }
   }
+  return pc;
+}
+// Plane p of the tile with its halo into registers; cells outside the domain
+// (or a plane outside [0, nz)) read as NaN.
+__device__ __forceinline__ void load_plane_regs(const float *__restrict__ g, int p,
+                                                const PlaneCells &pc, const GridP &G,
+                                                float (&r)[2]) {
+  const bool pin = p >= 0 && p < G.nz;
+  const float *gp = g + p * (G.nx * G.ny);
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    r[k] = (pin && pc.off[k] >= 0) ? gp[pc.off[k]] : __int_as_float(0x7fc00000);
 }
 __device__ __forceinline__ void store_plane_regs(float *sg, const float (&r)[2]) {
   const int tid = threadIdx.y * TX + threadIdx.x;
@@ -297,57 +311,60 @@ __device__ __forceinline__ void store_plane_regs(float *sg, const float (&r)[2])
   }
 }
 
-// flush one plane of shared marks into the global bitmap
-__device__ __forceinline__ void flush_plane(uint32_t *__restrict__ marks, const uint8_t *sm, int p,
-                                            int x0, int y0, bool interior, const GridP &G) {
-  const int tid = threadIdx.y * TX + threadIdx.x;
-  if (interior) {
-    int gx = x0 + threadIdx.x, gy = y0 + threadIdx.y;
-    bool bit = sm[(threadIdx.y + 1) * SX + threadIdx.x + 1] && gx < G.nx && gy < G.ny;
-    uint32_t w = __ballot_sync(0xffffffffu, bit);
-    if (threadIdx.x == 0 && w)
-      atomicOr(&marks[(size_t)(gy + G.ny * p) * G.W + (x0 >> 5)], w);
-    if (tid < PERIM) {
-      int ly, lx;
-      perim_cell(tid, ly, lx);
-      int hx = x0 - 1 + lx, hy = y0 - 1 + ly;
-      if (sm[ly * SX + lx] && hx >= 0 && hx < G.nx && hy >= 0 && hy < G.ny)
-        atomicOr(&marks[(size_t)(hy + G.ny * p) * G.W + (hx >> 5)], 1u << (hx & 31));
-    }
-  } else {
-    for (int c = tid; c < SP; c += NT) {
-      int ly = c / SX, lx = c - ly * SX;
-      int hx = x0 - 1 + lx, hy = y0 - 1 + ly;
-      if (sm[c] && hx >= 0 && hx < G.nx && hy >= 0 && hy < G.ny)
-        atomicOr(&marks[(size_t)(hy + G.ny * p) * G.W + (hx >> 5)], 1u << (hx & 31));
-    }
+// Shared marks of one plane buffer: for every row ly (0..SY-1) the 7 row masks
+// (dz, dy) a warp can produce; word [ly][k] is written by exactly one warp
+// (row ly-1-dy_k) in exactly one step (plane P-dz_k), so plain stores suffice.
+typedef unsigned long long u64;
+constexpr int KR = 7;  // (dz,dy) = (-1,-1) (-1,0) (0,-1) (0,0) (0,1) (1,0) (1,1)
+
+// Flush (and clear) plane buffer `rows` of plane p into the global bitmap.
+// One warp: lane ly < SY ORs the 7 words of row ly and issues at most 3
+// atomics (left halo bit, 32 interior bits, right halo bit).
+__device__ __forceinline__ void flush_plane(uint32_t *__restrict__ marks, u64 (*rows)[KR], int p,
+                                            int x0, int y0, const GridP &G) {
+  const int ly = threadIdx.x;
+  if (ly >= SY) return;
+  u64 val = 0;
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    val |= rows[ly][k];
+    rows[ly][k] = 0ull;
   }
+  const int gy = y0 - 1 + ly;
+  if (!val || gy < 0 || gy >= G.ny || p < 0 || p >= G.nz) return;
+  uint32_t *row = marks + (size_t)(gy + G.ny * p) * G.W;
+  const int wx = x0 >> 5;
+  const uint32_t w = (uint32_t)(val >> 1);
+  if (w) atomicOr(&row[wx], w);
+  if ((val & 1ull) && x0 > 0) atomicOr(&row[wx - 1], 0x80000000u);
+  if (((val >> 33) & 1ull) && x0 + 32 < G.nx) atomicOr(&row[wx + 1], 1u);
 }
 
 // R1, R2, R3 at every vertex from its closed star in g and its ref word;
 // writes the packed steepest slots (dn | up << 4) used by the label walks.
-__global__ void __launch_bounds__(NT) k_stencil(const float *__restrict__ g,
-                                                const uint32_t *__restrict__ ref,
-                                                uint32_t *__restrict__ marks,
-                                                uint8_t *__restrict__ slots, GridP G, int zc,
-                                                unsigned long long *cnt) {
+__global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
+                                                   const uint32_t *__restrict__ ref,
+                                                   uint32_t *__restrict__ marks,
+                                                   uint8_t *__restrict__ slots, GridP G, int zc,
+                                                   unsigned long long *cnt) {
   __shared__ float sg[4][SP];
-  __shared__ uint8_t sm[4][SP];
+  __shared__ u64 smk[4][SY][KR];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, G.nz);
+  const int z0 = G.zb + blockIdx.z * zc, z1 = min(z0 + zc, G.ze);
   const int x = x0 + tx, y = y0 + ty;
   const bool inside = x < G.nx && y < G.ny;
   const int c = (ty + 1) * SX + tx + 1;
   unsigned n1 = 0, n2 = 0, n3 = 0;
+  const PlaneCells pc = plane_cells(x0, y0, G);
 
   {  // prologue: planes z0-1, z0, z0+1 (NaN outside the domain), cleared marks
     float r[2];
     for (int p = z0 - 1; p <= z0 + 1; ++p) {
-      load_plane_regs(g, p, x0, y0, G, r);
+      load_plane_regs(g, p, pc, G, r);
       store_plane_regs(sg[p & 3], r);
     }
-    for (int k = tid; k < 4 * SP; k += NT) (&sm[0][0])[k] = 0;
+    for (int k = tid; k < 4 * SY * KR; k += NT) (&smk[0][0][0])[k] = 0ull;
   }
   __syncthreads();
 
@@ -355,21 +372,22 @@ __global__ void __launch_bounds__(NT) k_stencil(const float *__restrict__ g,
     float pre[2];
     const int pz = z + 2;
     const bool prefetch = pz <= z1;
-    if (prefetch) load_plane_regs(g, pz, x0, y0, G, pre);
+    if (prefetch) load_plane_regs(g, pz, pc, G, pre);
 
+    uint32_t tgt = 0;  // targets as a 15-bit mask over the closed star (bit 14 = self)
     if (inside) {
       const int i = x + G.nx * (y + G.ny * z);
+      const float *pm = &sg[(z - 1) & 3][c], *p0 = &sg[z & 3][c], *pp = &sg[(z + 1) & 3][c];
       float v[kSlots];
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {  // s is a compile-time constant here
         const int b = slot_bits(s), sg1 = slot_sign(s);
-        v[s] = sg[(z + sg1 * (b >> 2)) & 3][c + sg1 * ((b & 1) + ((b >> 1) & 1) * SX)];
+        const float *pl = (b >> 2) ? (sg1 > 0 ? pp : pm) : p0;
+        v[s] = pl[sg1 * ((b & 1) + ((b >> 1) & 1) * SX)];
       }
-      const float hc = sg[z & 3][c];
+      const float hc = *p0;
       const Star st = eval_values(v, hc);
       const uint32_t r = __ldcs(&ref[i]);
-      // targets as a 15-bit mask over the closed star (bit 14 = self)
-      uint32_t tgt = 0;
       // R1: the g-largest neighbour is an impostor -> decrease it
       if (st.up != ref_up(r)) { tgt |= 1u << st.up; n1 += 1; }
       // R2: the g-smallest neighbour changed -> decrease the true N_min
@@ -391,27 +409,45 @@ __global__ void __launch_bounds__(NT) k_stencil(const float *__restrict__ g,
           if (flip & ~flow) tgt |= 1u << kSelf;
         }
       }
-      for (; tgt; tgt &= tgt - 1) {
-        const int s = __ffs(tgt) - 1;
-        if (s == kSelf) {
-          sm[z & 3][c] = 1;
-        } else {
-          const int b = slot_bits(s), sg1 = slot_sign(s);
-          sm[(z + sg1 * (b >> 2)) & 3][c + sg1 * ((b & 1) + ((b >> 1) & 1) * SX)] = 1;
-        }
-      }
       if (slots) slots[i] = (uint8_t)(st.dn | (st.up << 4));
     }
+    // warp-aggregated marks: one ballot per slot, shifted into 7 row masks
+    if (__any_sync(0xffffffffu, tgt)) {
+      uint32_t bal[15];
+#pragma unroll
+      for (int s = 0; s < 15; ++s) bal[s] = __ballot_sync(0xffffffffu, (tgt >> s) & 1u);
+      // bit position = 1 + dx (lane 0 <-> lx 1)
+      const u64 rv[KR] = {
+          (u64)bal[0] | ((u64)bal[1] << 1),                        // (-1,-1): slots 0, 1
+          (u64)bal[2] | ((u64)bal[3] << 1),                        // (-1, 0): slots 2, 3
+          (u64)bal[4] | ((u64)bal[5] << 1),                        // ( 0,-1): slots 4, 5
+          (u64)bal[6] | ((u64)bal[14] << 1) | ((u64)bal[7] << 2),  // ( 0, 0): 6, self, 7
+          ((u64)bal[8] << 1) | ((u64)bal[9] << 2),                 // ( 0, 1): slots 8, 9
+          ((u64)bal[10] << 1) | ((u64)bal[11] << 2),               // ( 1, 0): slots 10, 11
+          ((u64)bal[12] << 1) | ((u64)bal[13] << 2)};              // ( 1, 1): slots 12, 13
+      if (tx < KR) {
+        const int dz = tx < 2 ? -1 : (tx < 5 ? 0 : 1);
+        const int dy = (tx == 0 || tx == 2) ? -1 : ((tx == 4 || tx == 6) ? 1 : 0);
+        u64 val = 0;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) val = (k == tx) ? rv[k] : val;
+        smk[(z + dz) & 3][ty + 1 + dy][tx] = val;
+      }
+    }
+    // plane z-2 is complete (its contributors z-3 .. z-1 are done): one warp
+    // flushes it
+    const int pf = z - 2;
+    if (ty == (z & (TY - 1)) && pf >= z0 - 1 && pf >= 0)
+      flush_plane(marks, smk[pf & 3], pf, x0, y0, G);
     if (prefetch) store_plane_regs(sg[pz & 3], pre);
-    for (int k = tid; k < SP; k += NT) sm[pz & 3][k] = 0;  // buffer of plane z-2 (flushed)
-    __syncthreads();
-    if (z - 1 >= z0) flush_plane(marks, sm[(z - 1) & 3], z - 1, x0, y0, true, G);
-    else if (z - 1 >= 0) flush_plane(marks, sm[(z - 1) & 3], z - 1, x0, y0, false, G);
     __syncthreads();
   }
-  // epilogue: the last interior plane and the halo plane above the chunk
-  if (z1 - 1 >= z0) flush_plane(marks, sm[(z1 - 1) & 3], z1 - 1, x0, y0, true, G);
-  if (z1 < G.nz) flush_plane(marks, sm[z1 & 3], z1, x0, y0, false, G);
+  // epilogue: planes z1-2 .. z1 not flushed by the loop (one warp each)
+  {
+    const int pf = z1 - 2 + ty;
+    if (ty < 3 && pf >= z0 - 1 && pf >= 0 && pf < G.nz)
+      flush_plane(marks, smk[pf & 3], pf, x0, y0, G);
+  }
 
   warp_add(&cnt[C_N1 + 0], n1);
   warp_add(&cnt[C_N1 + 1], n2);
@@ -436,20 +472,70 @@ __global__ void k_saddle_order(const float *__restrict__ g, const int32_t *__res
 
 // Terminus of the steepest path from u (O6): follow 4-bit slot pointers.
 // FROM_REF: pointers of f (ref word bits 14-17 / 18-21); else of g (slot
-// bytes written by the stencil, low / high nibble).
+// bytes written by the stencil, low / high nibble).  Returns the local root,
+// or -(w + 1) for the first vertex w of the path outside the owned planes
+// (sharded slabs only; on a single GPU every path stays inside).
 template <bool UP, bool FROM_REF>
 __device__ __forceinline__ int walk(int u, const uint8_t *__restrict__ slots,
                                     const uint32_t *__restrict__ ref, const GridP &G) {
+  const int A = G.nx * G.ny, lo = G.zb * A, hi = G.ze * A;
   int w = u;
   for (;;) {
+    if (w < lo || w >= hi) return -(w + 1);
     int s;
     if (FROM_REF) s = (__ldg(&ref[w]) >> (UP ? 18 : 14)) & 15;
     else s = (__ldg(&slots[w]) >> (UP ? 4 : 0)) & 15;
     if (s == kSelf) return w;
     const int b = slot_bits(s);
-    const int d = (b & 1) + ((b >> 1) & 1) * G.nx + (b >> 2) * G.nx * G.ny;
+    const int d = (b & 1) + ((b >> 1) & 1) * G.nx + (b >> 2) * A;
     w += slot_sign(s) * d;
   }
+}
+
+// Boundary tables of a sharded run (z-slabs): for every vertex of the first
+// and last owned plane of every rank, the terminus of its steepest path in
+// the rank's slab: {label, value bits} (a root) or {-(x+1), 0} (the path
+// leaves the slab at global vertex x, which lies in a neighbour's boundary
+// plane).  Gathered on every rank and resolved by pointer jumping: paths
+// strictly descend (ascend) in SoS order, so the chains are acyclic and the
+// resolved table is unique.
+struct Slabs {
+  const int *start;  // start[r] = global first plane of rank r, start[p] = gnz
+  int p;
+  const int2 *table;  // 2 * p * A resolved entries, or nullptr (single GPU)
+};
+
+__device__ __forceinline__ int2 table_entry(const Slabs &S, int xg, int A) {
+  const int z = xg / A;
+  int r = 0;
+  while (r + 1 < S.p && S.start[r + 1] <= z) ++r;
+  const int side = (z == S.start[r]) ? 0 : 1;
+  return S.table[(size_t)(2 * r + side) * A + (xg - z * A)];
+}
+
+template <bool UP, bool FROM_REF>
+__global__ void k_boundary_walks(const float *__restrict__ h, const uint8_t *__restrict__ slots,
+                                 const uint32_t *__restrict__ ref, GridP G, int2 *out) {
+  const int A = G.nx * G.ny;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * A) return;
+  const int side = i / A, xy = i - side * A;
+  const int v = (side ? G.ze - 1 : G.zb) * A + xy;
+  const int e = walk<UP, FROM_REF>(v, slots, ref, G);
+  const int off = G.zoff * A;
+  out[i] = e >= 0 ? make_int2(e + off, __float_as_int(h[e])) : make_int2(-(-e - 1 + off) - 1, 0);
+}
+
+__global__ void k_resolve(int2 *table, int n, Slabs S, int A, unsigned long long *changed) {
+  unsigned ch = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int2 e = table[i];
+    if (e.x >= 0) continue;
+    int2 e2 = table_entry(S, -e.x - 1, A);
+    table[i] = e2;
+    ch |= (e2.x < 0);
+  }
+  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(changed, 1ull);
 }
 
 // R5 / R6 (C3): for a join saddle s, m2 = <_h-largest minimum
@@ -458,40 +544,48 @@ __device__ __forceinline__ int walk(int u, const uint8_t *__restrict__ slots,
 // walking its own integral path; a 16-lane shuffle reduction picks the
 // extremum.  FROM_REF: h = f, the result is m1 / M1 (reference).
 // Else h = g: if the pick differs from m1 (M1), mark m2 (join) or
-// M1 (split, amb-12).
+// M1 (split, amb-12).  Saddle lists, m1/M1 and labels are global ids; paths
+// leaving a slab are completed from the resolved boundary table; targets
+// outside the slab go to `remote` (sharded only).
 template <bool SPLIT, bool FROM_REF>
 __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
                                                 const int32_t *__restrict__ sl, int n,
                                                 const uint8_t *__restrict__ slots,
                                                 const uint32_t *__restrict__ ref,
                                                 int32_t *ref_ext, uint32_t *marks, GridP G,
+                                                Slabs S, int32_t *remote,
                                                 unsigned long long *cnt) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = gt >> 4, l16 = threadIdx.x & 15;
   const bool active = k < n;
+  const int A = G.nx * G.ny, off = G.zoff * A;
   int best = -1;
   float bv = 0.0f;
-  int s = 0;
-  if (active) {
-    s = __ldg(&sl[k]);
-    if (l16 < kSlots) {
-      int x = s % G.nx, yz = s / G.nx, y = yz % G.ny, z = yz / G.ny;
-      uint32_t valid = valid_mask(x, y, z, G);
-      if (valid & (1u << l16)) {
-        int u = s + G.delta[l16];
-        float hs = h[s], hu = h[u];
-        bool lower = (l16 < 7) ? (hu <= hs) : (hu < hs);
-        if (lower != SPLIT) {
-          best = walk<SPLIT, FROM_REF>(u, slots, ref, G);
-          bv = h[best];
+  if (active && l16 < kSlots) {
+    const int s = __ldg(&sl[k]) - off;  // local
+    const int x = s % G.nx, yz = s / G.nx, y = yz % G.ny, z = yz / G.ny;
+    const uint32_t valid = valid_mask(x, y, z, G);
+    if (valid & (1u << l16)) {
+      const int u = s + G.delta[l16];
+      const float hs = h[s], hu = h[u];
+      const bool lower = (l16 < 7) ? (hu <= hs) : (hu < hs);
+      if (lower != SPLIT) {
+        const int e = walk<SPLIT, FROM_REF>(u, slots, ref, G);
+        if (e >= 0) {
+          best = e + off;
+          bv = h[e];
+        } else {
+          const int2 t = table_entry(S, -e - 1 + off, A);
+          best = t.x;
+          bv = __int_as_float(t.y);
         }
       }
     }
   }
 #pragma unroll
-  for (int off = 8; off >= 1; off >>= 1) {
-    int ob = __shfl_xor_sync(0xffffffffu, best, off);
-    float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+  for (int o = 8; o >= 1; o >>= 1) {
+    int ob = __shfl_xor_sync(0xffffffffu, best, o);
+    float ov = __shfl_xor_sync(0xffffffffu, bv, o);
     bool take;
     if (ob < 0) take = false;
     else if (best < 0) take = true;
@@ -504,14 +598,66 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
     if (FROM_REF) {
       ref_ext[k] = best;
     } else {
-      int want = ref_ext[k];
+      const int want = ref_ext[k];
       if (best >= 0 && best != want) {
-        mark_vertex(marks, SPLIT ? want : best, G);
+        const int t = (SPLIT ? want : best) - off;
+        if (t >= G.zb * A && t < G.ze * A) mark_vertex(marks, t, G);
+        else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = t + off;
         hit = 1;
       }
     }
   }
   if (!FROM_REF) warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
+}
+
+// ------------------------------------------------ sharded helpers (z-slabs)
+// R4 with the replicated saddle values gS (uint32 bit patterns, S order):
+// the owner of S[k] checks the pair (S[k], S[k+1]).
+__global__ void k_saddle_order_slab(const uint32_t *__restrict__ gS,
+                                    const int32_t *__restrict__ S, int nS, uint32_t *marks,
+                                    GridP G, unsigned long long *cnt) {
+  unsigned n4 = 0;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int A = G.nx * G.ny, off = G.zoff * A;
+  if (k + 1 < nS) {
+    const int a = S[k] - off;
+    if (a >= G.zb * A && a < G.ze * A) {
+      const float va = __int_as_float(gS[k]), vb = __int_as_float(gS[k + 1]);
+      if (vb < va || (vb == va && S[k + 1] < S[k])) {
+        mark_vertex(marks, a, G);
+        n4 = 1;
+      }
+    }
+  }
+  warp_add(&cnt[C_N1 + 3], n4);
+}
+
+// gS[k] = bits of g at S[k] for owned saddles, 0 elsewhere (max-all-reduced)
+__global__ void k_fill_gS(const float *__restrict__ g, const int32_t *__restrict__ S, int nS,
+                          uint32_t *gS, GridP G) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nS) return;
+  const int A = G.nx * G.ny, a = S[k] - G.zoff * A;
+  gS[k] = (a >= G.zb * A && a < G.ze * A) ? __float_as_uint(g[a]) : 0u;
+}
+
+// apply gathered remote marks (global ids) that this slab owns
+__global__ void k_apply_remote(const int32_t *__restrict__ ids, int n, uint32_t *marks, GridP G) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int A = G.nx * G.ny, t = ids[k] - G.zoff * A;
+  if (t >= G.zb * A && t < G.ze * A) mark_vertex(marks, t, G);
+}
+
+__global__ void k_or_words(uint32_t *__restrict__ dst, const uint32_t *__restrict__ src, int n) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n && src[k]) atomicOr(&dst[k], src[k]);
+}
+
+// local ids -> global ids
+__global__ void k_add_offset(int32_t *ids, int n, int off) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) ids[k] += off;
 }
 
 // ---------------------------------------------------- count + edit (O9)
@@ -546,11 +692,12 @@ __global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
                                                     float xi, float delta, int N, int do_edit,
                                                     unsigned long long *cnt) {
   const int lane = threadIdx.x & 31;
-  const int64_t nwords = (int64_t)G.ny * G.nz * G.W;
+  const int64_t nwords = (int64_t)G.ny * G.ze * G.W;  // owned rows: [zb*ny, ze*ny)
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned vt = 0, ap = 0;
-  for (int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4; w0 < nwords;
-       w0 += nwarps * 4) {
+  for (int64_t w0 = (int64_t)G.ny * G.zb * G.W +
+                    (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4;
+       w0 < nwords; w0 += nwarps * 4) {
     // lanes 0..3 fetch the 4 words of this batch; broadcast by shuffle
     uint32_t mine = (lane < 4 && w0 + lane < nwords) ? marks[w0 + lane] : 0u;
 #pragma unroll

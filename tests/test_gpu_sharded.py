@@ -1,0 +1,73 @@
+"""The z-slab decomposition is bit-equal to the single-GPU call.
+
+exactz_correct_slabs runs the sharded algorithm — ghost planes, replicated
+saddle values, gathered boundary tables for cross-slab label walks, remote
+marks, all-reduced counters — with N virtual ranks on one GPU (loopback
+transport instead of NCCL).  Same bar as the single-GPU parity: out, edit
+counts, iteration count and every per-pass counter bit-equal, for slab counts
+that leave 1-plane slabs and ragged splits."""
+import numpy as np
+import pytest
+import torch
+
+from synth import fields as S
+
+pytestmark = pytest.mark.gpu
+
+
+def both(E, f, g, xi, p, **kw):
+    fd, gd = f.cuda(), g.cuda()
+    c1 = torch.empty(f.numel(), dtype=torch.uint8, device="cuda")
+    c2 = torch.empty_like(c1)
+    a = E.exactz_correct(fd, gd, xi, edit_counts=c1, stats_cap=100000, **kw)
+    b = E.exactz_correct_slabs(fd, gd, xi, p, edit_counts=c2, stats_cap=100000, **kw)
+    torch.cuda.synchronize()
+    return a, b, c1, c2
+
+
+def assert_same(a, b, c1, c2):
+    assert b.status == a.status and b.iters == a.iters
+    assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
+    assert torch.equal(c1, c2)
+    assert a.stats == b.stats
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 16])
+def test_slabs_c1(exactz, p):
+    f, g, xi = S.make("C1")
+    assert_same(*both(exactz, f, g, xi, p))
+
+
+@pytest.mark.parametrize("cfg,shape,p", [("C2", (20, 24, 70), 4), ("C3", (17, 21, 40), 3),
+                                         ("C5", (9, 12, 33), 8), ("C3", (12, 16, 50), 12)])
+def test_slabs_configs(exactz, cfg, shape, p):
+    f, g, xi = S.make(cfg, shape=shape)
+    assert_same(*both(exactz, f, g, xi, p))
+
+
+def test_slabs_sz_plateaus(exactz):
+    f, g, xi = S.make("C3", shape=(10, 14, 45), mode="sz")
+    assert_same(*both(exactz, f, g, xi, 4))
+
+
+def test_slabs_flags_and_max_iters(exactz):
+    f, g, xi = S.make("C1")
+    for kw in ({"flags": 1}, {"flags": 2}, {"max_iters": 2}, {"N": 2}):
+        assert_same(*both(exactz, f, g, xi, 3, **kw))
+
+
+def test_slabs_match_oracle(exactz, oracle):
+    f, g, xi = S.make("C2", shape=(14, 10, 30))
+    r = oracle.correct(f.numpy(), g.numpy(), xi, 5)
+    b = exactz.exactz_correct_slabs(f.cuda(), g.cuda(), xi, 5)
+    assert b.iters == r.iters
+    assert np.array_equal(b.out.cpu().numpy().reshape(-1).view(np.uint32), r.out.view(np.uint32))
+
+
+def test_slabs_errors(exactz):
+    f, g, xi = S.make("C1")
+    E = exactz
+    assert E.status_of(E.exactz_correct_slabs, f.cuda(), g.cuda(), xi, 17) == E.EINVAL  # nz < p
+    bad = g.clone()
+    bad.view(-1)[7] = f.view(-1)[7] + 3 * xi
+    assert E.status_of(E.exactz_correct_slabs, f.cuda(), bad.cuda(), xi, 2) == E.EBOUND
