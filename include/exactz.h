@@ -83,6 +83,7 @@ typedef struct {
                           R3 flipped (vertex, link-vertex) pairs at saddles / type
                           changes, R4 flipped adjacent saddles, R5 join events,
                           R6 split events */
+  uint64_t walk_steps; /* diagnostic: steps of the C3 label walks in this pass */
 } exactz_iter_stats;
 
 typedef struct {

@@ -26,7 +26,8 @@ if not os.path.exists(LIB_PATH):
 
 
 class IterStats(C.Structure):
-    _fields_ = [("violations", C.c_uint64), ("applied", C.c_uint64), ("n", C.c_uint64 * 6)]
+    _fields_ = [("violations", C.c_uint64), ("applied", C.c_uint64), ("n", C.c_uint64 * 6),
+                ("walk_steps", C.c_uint64)]
 
 
 class Stats(C.Structure):
@@ -142,9 +143,12 @@ def _opts(N, max_iters, flags, edit_counts, label_min, label_max, stats_cap):
 def _result(status, iters, st, rows):
     n = min(st.nrows, st.cap)
     table = [(r.violations, r.applied, *list(r.n)) for r in rows[:n]] if st.cap else []
+    walks = [int(r.walk_steps) for r in rows[:n]] if st.cap else []
     kern = {KERNEL_CLASSES[k]: (st.kernel_ms[k], int(st.kernel_launches[k]),
                                 int(st.kernel_bytes[k])) for k in range(8)}
-    return CorrectResult(status, iters.value, table, st.ms_setup, st.ms_loop, kern)
+    res = CorrectResult(status, iters.value, table, st.ms_setup, st.ms_loop, kern)
+    res.walk_steps = walks
+    return res
 
 
 def exactz_correct(f, g_in, eps: float, out=None, *, N: int = 5, max_iters: int = 0,

@@ -323,7 +323,7 @@ static void build_reference(Ctx &C, const float *f, Reference &R) {
 }
 
 struct PassOut {
-  unsigned long long vt, applied, n[6];
+  unsigned long long vt, applied, n[6], walk;
 };
 
 // One CheckConstraints pass on g (O8) followed by the count and, when
@@ -359,6 +359,7 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
   o.applied = C.hcnt[C_APPLIED];
   C.prof.bytes[EXACTZ_K_EDIT] += 14ull * o.applied;  // f, g, c read; g, c written
   for (int k = 0; k < 6; ++k) o.n[k] = C.hcnt[C_N1 + k];
+  o.walk = C.hcnt[C_WALK];
   return o;
 }
 
@@ -421,6 +422,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       r.violations = o.vt;
       r.applied = o.applied;
       for (int k = 0; k < 6; ++k) r.n[k] = o.n[k];
+      r.walk_steps = o.walk;
     }
     ++rows;
     if (o.vt == 0) break;
@@ -546,6 +548,7 @@ exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3]
       row->violations = o.vt;
       row->applied = 0;
       for (int k = 0; k < 6; ++k) row->n[k] = o.n[k];
+      row->walk_steps = o.walk;
     }
     CK(cudaStreamSynchronize(s));
     return EXACTZ_OK;

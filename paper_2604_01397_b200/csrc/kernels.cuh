@@ -41,6 +41,7 @@ enum Counter {
   C_KEYMIN = 12,  // eps_from_relative: ordered-key min / max
   C_KEYMAX = 13,
   C_NREMOTE = 14,  // sharded: remote marks appended by k_events
+  C_WALK = 15,     // diagnostic: steps taken by the label walks of a pass
   C_NCOUNTERS = 16
 };
 
@@ -477,10 +478,11 @@ __global__ void k_saddle_order(const float *__restrict__ g, const int32_t *__res
 // (sharded slabs only; on a single GPU every path stays inside).
 template <bool UP, bool FROM_REF>
 __device__ __forceinline__ int walk(int u, const uint8_t *__restrict__ slots,
-                                    const uint32_t *__restrict__ ref, const GridP &G) {
+                                    const uint32_t *__restrict__ ref, const GridP &G,
+                                    unsigned &steps) {
   const int A = G.nx * G.ny, lo = G.zb * A, hi = G.ze * A;
   int w = u;
-  for (;;) {
+  for (;; ++steps) {
     if (w < lo || w >= hi) return -(w + 1);
     int s;
     if (FROM_REF) s = (__ldg(&ref[w]) >> (UP ? 18 : 14)) & 15;
@@ -521,7 +523,8 @@ __global__ void k_boundary_walks(const float *__restrict__ h, const uint8_t *__r
   if (i >= 2 * A) return;
   const int side = i / A, xy = i - side * A;
   const int v = (side ? G.ze - 1 : G.zb) * A + xy;
-  const int e = walk<UP, FROM_REF>(v, slots, ref, G);
+  unsigned steps = 0;
+  const int e = walk<UP, FROM_REF>(v, slots, ref, G, steps);
   const int off = G.zoff * A;
   out[i] = e >= 0 ? make_int2(e + off, __float_as_int(h[e])) : make_int2(-(-e - 1 + off) - 1, 0);
 }
@@ -561,6 +564,7 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
   const int A = G.nx * G.ny, off = G.zoff * A;
   int best = -1;
   float bv = 0.0f;
+  unsigned steps = 0;
   if (active && l16 < kSlots) {
     const int s = __ldg(&sl[k]) - off;  // local
     const int x = s % G.nx, yz = s / G.nx, y = yz % G.ny, z = yz / G.ny;
@@ -570,7 +574,7 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
       const float hs = h[s], hu = h[u];
       const bool lower = (l16 < 7) ? (hu <= hs) : (hu < hs);
       if (lower != SPLIT) {
-        const int e = walk<SPLIT, FROM_REF>(u, slots, ref, G);
+        const int e = walk<SPLIT, FROM_REF>(u, slots, ref, G, steps);
         if (e >= 0) {
           best = e + off;
           bv = h[e];
@@ -608,6 +612,7 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
     }
   }
   if (!FROM_REF) warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
+  if (!FROM_REF) warp_add(&cnt[C_WALK], steps);
 }
 
 // ------------------------------------------------ sharded helpers (z-slabs)
