@@ -62,6 +62,8 @@ typedef enum {
 #define EXACTZ_NO_C3 0x2u   /* debug: skip the event rules (C3, R5/R6) */
 #define EXACTZ_PROFILE 0x4u /* time every kernel class with CUDA events on `stream`
                                (exactz_stats.kernel_ms); results are unchanged */
+#define EXACTZ_NO_TRACK 0x8u /* debug: dense passes only (no change tracking; results
+                                are identical) */
 
 /* kernel classes reported by EXACTZ_PROFILE */
 enum {
@@ -83,7 +85,7 @@ typedef struct {
                           R3 flipped (vertex, link-vertex) pairs at saddles / type
                           changes, R4 flipped adjacent saddles, R5 join events,
                           R6 split events */
-  uint64_t walk_steps; /* diagnostic: steps of the C3 label walks in this pass */
+  uint64_t walk_steps; /* reserved for diagnostics (0 in this build) */
 } exactz_iter_stats;
 
 typedef struct {

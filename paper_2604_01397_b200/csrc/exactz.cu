@@ -260,14 +260,22 @@ struct Reference {
 
 template <bool SPLIT, bool FROM_REF>
 static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, const uint8_t *slots,
-                          const uint32_t *ref, int32_t *ext, uint32_t *marks) {
+                          const uint32_t *ref, int32_t *ext, uint32_t *marks,
+                          EvCache ec = EvCache{}, Track tr = Track{}) {
   if (n <= 0) return;
   int64_t threads = (int64_t)n * 16;
   // algorithmic bytes: per saddle its id, its value, 14 link values, the
   // reached extrema's values and ids
   C.run(FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS, 128ull * n, true, [&] {
-    k_events<SPLIT, FROM_REF><<<(unsigned)((threads + 255) / 256), 256, 0, C.s>>>(
-        h, sl, n, slots, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt);
+    const unsigned blocks = (unsigned)((threads + 255) / 256);
+    if (ec.rnd)
+      k_events<SPLIT, FROM_REF, true, false><<<blocks, 256, 0, C.s>>>(
+          h, sl, n, slots, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, ec, tr,
+          C.cnt);
+    else
+      k_events<SPLIT, FROM_REF, false, false><<<blocks, 256, 0, C.s>>>(
+          h, sl, n, slots, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, ec, tr,
+          C.cnt);
   });
 }
 
@@ -328,16 +336,91 @@ struct PassOut {
 
 // One CheckConstraints pass on g (O8) followed by the count and, when
 // do_edit, the bounded edits (O9).  slots receives g's steepest slots.
+// Change-tracking state of a call (single GPU, late passes; kernels.cuh Track).
+struct Tracking {
+  // vertex activity: act[cur] = this pass's active set (valid when `ready`)
+  bool act_on = false, ready = false;
+  uint32_t *act[2] = {nullptr, nullptr};
+  int cur = 0;
+  // C3 cache with brick stamps
+  bool cache_on = false;
+  int nbx = 0, nby = 0, nbz = 0, nb = 0;
+  uint16_t *bval = nullptr, *bslot = nullptr;
+  EvCache ecJ{}, ecP{};
+  void geometry(const Ctx &C) {
+    nbx = (C.G.nx + BX - 1) / BX;
+    nby = (C.G.ny + BY - 1) / BY;
+    nbz = (C.G.nz + BZ - 1) / BZ;
+    nb = nbx * nby * nbz;
+  }
+  void start_act(Ctx &C) {
+    for (int k = 0; k < 2; ++k) {
+      act[k] = C.arena.get<uint32_t>(C.mark_words());
+      CK(cudaMemsetAsync(act[k], 0, C.mark_words() * 4, C.s));
+    }
+    act_on = true;
+  }
+  void start_cache(Ctx &C, const Reference &R) {
+    uint16_t *st = C.arena.get<uint16_t>(2 * (size_t)nb);
+    CK(cudaMemsetAsync(st, 0, 2 * (size_t)nb * 2, C.s));
+    bval = st;
+    bslot = st + nb;
+    auto cache = [&](int n) {
+      EvCache e;
+      e.rnd = C.arena.get<uint16_t>(n);
+      e.mask = C.arena.get<uint32_t>(n);
+      e.tgt = C.arena.get<int32_t>(n);
+      CK(cudaMemsetAsync(e.rnd, 0, (size_t)(n ? n : 1) * 2, C.s));
+      return e;
+    };
+    ecJ = cache(R.nJ);
+    ecP = cache(R.nP);
+    cache_on = true;
+  }
+  Track track(int round) const {
+    Track T{};
+    T.nbx = nbx;
+    T.nby = nby;
+    T.nbz = nbz;
+    T.round = round;
+    if (cache_on) {
+      T.bval = bval;
+      T.bslot = bslot;
+    }
+    if (act_on) T.act_next = act[cur ^ 1];
+    return T;
+  }
+};
+
+// One CheckConstraints pass on g (O8) followed by the count and, when
+// do_edit, the bounded edits (O9).  slots receives g's steepest slots.
+// With tracking: a sparse pass re-evaluates only the active vertices, and
+// cached C3 results are reused while their bricks are unchanged (exact; see
+// kernels.cuh Track).
 static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float *g, uint8_t *c,
                                uint32_t *marks, uint8_t *slots, float xi, float delta, int N,
-                               uint32_t flags, bool do_edit) {
+                               uint32_t flags, bool do_edit, Tracking *trk = nullptr,
+                               int round = 0) {
   bool c3 = !(flags & EXACTZ_NO_C3);
   C.zero();
+  const Track T = trk ? trk->track(round) : Track{};
+  const bool sparse = trk && trk->ready;
   // algorithmic bytes per vertex: g 4 + ref 4 read, slots 1 + mark bits 1/8
-  // written
-  C.run(EXACTZ_K_STENCIL, (uint64_t)C.V * 73 / 8, true, [&] {
-    k_stencil<<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, C.G, C.zc, C.cnt);
-  });
+  // written; a sparse pass: the active vertices only
+  if (!sparse) {
+    C.run(EXACTZ_K_STENCIL, (uint64_t)C.V * 73 / 8, true, [&] {
+      if (trk)
+        k_stencil<true><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, C.G, C.zc, T, C.cnt);
+      else
+        k_stencil<false><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, C.G, C.zc, T,
+                                                        C.cnt);
+    });
+  } else {
+    C.run(EXACTZ_K_STENCIL, (uint64_t)C.V / 8, true, [&] {
+      k_stencil_sparse<<<148 * 8, 256, 0, C.s>>>(g, R.ref, marks, slots, trk->act[trk->cur],
+                                                 C.G, T, C.cnt);
+    });
+  }
   if (!(flags & EXACTZ_NO_C2) && R.nS > 1) {
     C.run(EXACTZ_K_SADDLE_ORDER, 8ull * R.nS, true, [&] {
       k_saddle_order<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(g, R.S, R.nS, marks, C.G,
@@ -345,15 +428,26 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
     });
   }
   if (c3) {
-    launch_events<false, false>(C, g, R.J, R.nJ, slots, R.ref, R.m1, marks);
-    launch_events<true, false>(C, g, R.P, R.nP, slots, R.ref, R.M1, marks);
+    const bool cache = trk && trk->cache_on;
+    launch_events<false, false>(C, g, R.J, R.nJ, slots, R.ref, R.m1, marks,
+                                cache ? trk->ecJ : EvCache{}, T);
+    launch_events<true, false>(C, g, R.P, R.nP, slots, R.ref, R.M1, marks,
+                               cache ? trk->ecP : EvCache{}, T);
   }
   // bytes: mark words read (the per-edit 14 B are added once V_t is known)
   C.run(EXACTZ_K_EDIT, (uint64_t)C.V / 8, true, [&] {
-    k_count_edit<<<148 * 8, 256, 0, C.s>>>(g, c, marks, f, C.G, xi, delta, N, do_edit ? 1 : 0,
-                                           C.cnt);
+    if (trk)
+      k_count_edit<true><<<148 * 8, 256, 0, C.s>>>(g, c, marks, f, C.G, xi, delta, N,
+                                                   do_edit ? 1 : 0, T, C.cnt);
+    else
+      k_count_edit<false><<<148 * 8, 256, 0, C.s>>>(g, c, marks, f, C.G, xi, delta, N,
+                                                    do_edit ? 1 : 0, T, C.cnt);
   });
   C.read();
+  if (trk && trk->act_on) {  // act_next is complete: it is the next pass's set
+    trk->cur ^= 1;
+    trk->ready = true;
+  }
   PassOut o;
   o.vt = C.hcnt[C_VT];
   o.applied = C.hcnt[C_APPLIED];
@@ -414,9 +508,25 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   const float delta = eps / (float)N;  // Delta = RN(xi / N)
   uint32_t it = 0, rows = 0;
   exactz_status st = EXACTZ_OK;
+  Tracking trk;
+  trk.geometry(C);
+  unsigned long long prev_vt = (unsigned long long)V;
+  const bool allow_track = !(flags & EXACTZ_NO_TRACK);
   for (;;) {
     bool may_edit = !(max_iters && it >= max_iters);
-    PassOut o = detect_and_edit(C, R, f, out, c, marks, slots, eps, delta, N, flags, may_edit);
+    const int round = (int)rows + 1;  // stamps are 16-bit pass numbers
+    if (allow_track && rows >= 1 && round < 65000) {
+      // vertex activity once < 1/64 of the vertices are marked; the C3 cache
+      // once the marks are sparse at brick scale
+      if (!(flags & 0x10u) && !trk.act_on && prev_vt * 64 <= (unsigned long long)V)
+        trk.start_act(C);
+      if (!(flags & 0x20u) && !trk.cache_on && prev_vt * 32 <= (unsigned long long)trk.nb)
+        trk.start_cache(C, R);
+    }
+    const bool tracked = allow_track && round < 65000 && (trk.act_on || trk.cache_on);
+    PassOut o = detect_and_edit(C, R, f, out, c, marks, slots, eps, delta, N, flags, may_edit,
+                                tracked ? &trk : nullptr, round);
+    prev_vt = o.vt;
     if (stats && stats->rows && rows < stats->cap) {
       exactz_iter_stats &r = stats->rows[rows];
       r.violations = o.vt;

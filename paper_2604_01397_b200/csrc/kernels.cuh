@@ -57,6 +57,25 @@ struct GridP {
   int zb, ze;         // owned local planes [zb, ze)
 };
 
+// Change tracking (single GPU, late rounds).
+//  * Vertex activity: a vertex whose closed star saw no value change and that
+//    did not fire R1-R3 in the previous pass evaluates exactly as before (no
+//    fire, same steepest slots), so only act = St(edited) u fired is re-run,
+//    by the sparse stencil.  act_next collects the set for the next pass
+//    (bitmaps in the mark layout).
+//  * Brick stamps for the C3 cache: bricks of 32 x 8 x 8 vertices carry
+//      bval[b]  = pass in which a value change inside b becomes visible
+//                 (edits of pass t are stamped t + 1),
+//      bslot[b] = pass in which a steepest slot inside b changed;
+//    a saddle's cached C3 result is reused while no brick its walks touched
+//    changed.
+constexpr int BX = 32, BY = 8, BZ = 8;
+struct Track {
+  uint16_t *bval, *bslot;       // brick stamps (nullptr: C3 cache off)
+  uint32_t *act_next;           // vertex activity for the next pass (nullptr: off)
+  int nbx, nby, nbz, round;
+};
+
 // ref word layout (one uint32 per vertex, computed once from f):
 //   bits  0-13  f-lower mask (slot s set <=> neighbour s <_f i)
 //   bits 14-17  dn_f slot (0..13, 14 = self)
@@ -343,16 +362,18 @@ __device__ __forceinline__ void flush_plane(uint32_t *__restrict__ marks, u64 (*
 
 // R1, R2, R3 at every vertex from its closed star in g and its ref word;
 // writes the packed steepest slots (dn | up << 4) used by the label walks.
+template <bool TRACK>
 __global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
                                                    const uint32_t *__restrict__ ref,
                                                    uint32_t *__restrict__ marks,
                                                    uint8_t *__restrict__ slots, GridP G, int zc,
-                                                   unsigned long long *cnt) {
+                                                   Track T, unsigned long long *cnt) {
   __shared__ float sg[4][SP];
   __shared__ u64 smk[4][SY][KR];
+  const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = G.zb + blockIdx.z * zc, z1 = min(z0 + zc, G.ze);
+  const int x0 = bx * TX, y0 = by * TY;
+  const int z0 = G.zb + bz * zc, z1 = min(z0 + zc, G.ze);
   const int x = x0 + tx, y = y0 + ty;
   const bool inside = x < G.nx && y < G.ny;
   const int c = (ty + 1) * SX + tx + 1;
@@ -376,6 +397,7 @@ __global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
     if (prefetch) load_plane_regs(g, pz, pc, G, pre);
 
     uint32_t tgt = 0;  // targets as a 15-bit mask over the closed star (bit 14 = self)
+    bool schg = false;
     if (inside) {
       const int i = x + G.nx * (y + G.ny * z);
       const float *pm = &sg[(z - 1) & 3][c], *p0 = &sg[z & 3][c], *pp = &sg[(z + 1) & 3][c];
@@ -410,7 +432,18 @@ __global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
           if (flip & ~flow) tgt |= 1u << kSelf;
         }
       }
-      if (slots) slots[i] = (uint8_t)(st.dn | (st.up << 4));
+      const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
+      if (TRACK && T.bval) schg = (slots[i] != ns);
+      slots[i] = ns;
+    }
+    if (TRACK && T.bval) {  // slot-change stamp of this warp's brick
+      const unsigned chg = __ballot_sync(0xffffffffu, schg);
+      if (tx == 0 && chg) T.bslot[bx + T.nbx * ((y / BY) + T.nby * (z / BZ))] = (uint16_t)T.round;
+      schg = false;
+    }
+    if (TRACK && T.act_next) {  // fired vertices stay active next pass
+      const unsigned fired = __ballot_sync(0xffffffffu, tgt != 0);
+      if (tx == 0 && fired) atomicOr(&T.act_next[(size_t)(y + G.ny * z) * G.W + bx], fired);
     }
     // warp-aggregated marks: one ballot per slot, shifted into 7 row masks
     if (__any_sync(0xffffffffu, tgt)) {
@@ -455,6 +488,69 @@ __global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
   warp_add(&cnt[C_N1 + 2], n3);
 }
 
+// Sparse pass (tracking): re-evaluate only the active vertices (warp per
+// 32-bit word of the activity bitmap, consumed words are cleared).  Same
+// rules as k_stencil, neighbour values read from global memory.
+__global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict__ g,
+                                                        const uint32_t *__restrict__ ref,
+                                                        uint32_t *__restrict__ marks,
+                                                        uint8_t *__restrict__ slots,
+                                                        uint32_t *__restrict__ act, GridP G,
+                                                        Track T, unsigned long long *cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)G.ny * G.zb * G.W, nwords = (int64_t)G.ny * G.ze * G.W;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned n1 = 0, n2 = 0, n3 = 0;
+  for (int64_t w = w0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w < nwords;
+       w += nwarps) {
+    const uint32_t word = act[w];
+    if (!word) continue;
+    if (lane == 0) act[w] = 0u;
+    const int row = (int)(w / G.W), wx = (int)(w - (int64_t)row * G.W);
+    const int y = row % G.ny, z = row / G.ny, x = wx * 32 + lane;
+    uint32_t tgt = 0;
+    bool schg = false;
+    if (((word >> lane) & 1u) && x < G.nx) {
+      const int i = x + G.nx * row;
+      const uint32_t valid = valid_mask(x, y, z, G);
+      const Star st = eval_star(g, i, valid, G);
+      const uint32_t r = ref[i];
+      if (st.up != ref_up(r)) { tgt |= 1u << st.up; n1 += 1; }
+      if (st.dn != ref_dn(r)) { tgt |= 1u << ref_dn(r); n2 += 1; }
+      const uint32_t flow = ref_flow(r);
+      const uint32_t flip = st.lower ^ flow;
+      if (flip) {
+        bool apply = ref_saddle(r);
+        if (!apply) {
+          int nl, nu;
+          link_type(st.lower, valid, nl, nu);
+          apply = (nl != ref_nlc(r)) || (nu != ref_nuc(r));
+        }
+        if (apply) {
+          n3 += __popc(flip);
+          tgt |= flip & flow;
+          if (flip & ~flow) tgt |= 1u << kSelf;
+        }
+      }
+      for (uint32_t m = tgt; m; m &= m - 1) mark_vertex(marks, slot_target(i, __ffs(m) - 1, G), G);
+      const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
+      schg = slots[i] != ns;
+      slots[i] = ns;
+    }
+    if (T.bval) {
+      const unsigned chg = __ballot_sync(0xffffffffu, schg);
+      if (lane == 0 && chg) T.bslot[wx + T.nbx * ((y / BY) + T.nby * (z / BZ))] = (uint16_t)T.round;
+    }
+    if (T.act_next) {
+      const unsigned fired = __ballot_sync(0xffffffffu, tgt != 0);
+      if (lane == 0 && fired) atomicOr(&T.act_next[w], fired);
+    }
+  }
+  warp_add(&cnt[C_N1 + 0], n1);
+  warp_add(&cnt[C_N1 + 1], n2);
+  warp_add(&cnt[C_N1 + 2], n3);
+}
+
 // R4 (C2): adjacent saddles a = S[k] <_f b = S[k+1]; if b <_g a,
 // decrease a (the f-smaller).
 __global__ void k_saddle_order(const float *__restrict__ g, const int32_t *__restrict__ S,
@@ -476,14 +572,13 @@ __global__ void k_saddle_order(const float *__restrict__ g, const int32_t *__res
 // bytes written by the stencil, low / high nibble).  Returns the local root,
 // or -(w + 1) for the first vertex w of the path outside the owned planes
 // (sharded slabs only; on a single GPU every path stays inside).
-template <bool UP, bool FROM_REF>
+template <bool UP, bool FROM_REF, bool SLAB>
 __device__ __forceinline__ int walk(int u, const uint8_t *__restrict__ slots,
-                                    const uint32_t *__restrict__ ref, const GridP &G,
-                                    unsigned &steps) {
+                                    const uint32_t *__restrict__ ref, const GridP &G) {
   const int A = G.nx * G.ny, lo = G.zb * A, hi = G.ze * A;
   int w = u;
-  for (;; ++steps) {
-    if (w < lo || w >= hi) return -(w + 1);
+  for (;;) {
+    if (SLAB && (w < lo || w >= hi)) return -(w + 1);
     int s;
     if (FROM_REF) s = (__ldg(&ref[w]) >> (UP ? 18 : 14)) & 15;
     else s = (__ldg(&slots[w]) >> (UP ? 4 : 0)) & 15;
@@ -523,8 +618,7 @@ __global__ void k_boundary_walks(const float *__restrict__ h, const uint8_t *__r
   if (i >= 2 * A) return;
   const int side = i / A, xy = i - side * A;
   const int v = (side ? G.ze - 1 : G.zb) * A + xy;
-  unsigned steps = 0;
-  const int e = walk<UP, FROM_REF>(v, slots, ref, G, steps);
+  const int e = walk<UP, FROM_REF, true>(v, slots, ref, G);
   const int off = G.zoff * A;
   out[i] = e >= 0 ? make_int2(e + off, __float_as_int(h[e])) : make_int2(-(-e - 1 + off) - 1, 0);
 }
@@ -541,6 +635,43 @@ __global__ void k_resolve(int2 *table, int n, Slabs S, int A, unsigned long long
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(changed, 1ull);
 }
 
+// Per-saddle cache of the C3 result (tracking mode).  rnd = round it was
+// computed in (0: none), mask = the bricks (relative to the saddle's brick,
+// bit (dz+1)*9 + (dy+1)*3 + (dx+1)) holding the saddle's star, every walked
+// vertex and the reached extrema; bit 31 = some vertex outside that 3x3x3
+// neighbourhood (never reused); tgt = the marked target or -1.
+struct EvCache {
+  uint16_t *rnd;
+  uint32_t *mask;
+  int32_t *tgt;
+};
+
+__device__ __forceinline__ void brick_bit(int x, int y, int z, int bsx, int bsy, int bsz,
+                                          uint32_t &mask) {
+  const int dx = (x / BX) - bsx, dy = (y / BY) - bsy, dz = (z / BZ) - bsz;
+  if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) mask |= 0x80000000u;
+  else mask |= 1u << ((dz + 1) * 9 + (dy + 1) * 3 + (dx + 1));
+}
+
+// walk() that also records the bricks it visits (single GPU, g slots)
+template <bool UP>
+__device__ __forceinline__ int walk_track(int u, int x, int y, int z,
+                                          const uint8_t *__restrict__ slots, const GridP &G,
+                                          int bsx, int bsy, int bsz, uint32_t &mask) {
+  const int A = G.nx * G.ny;
+  int w = u;
+  for (;;) {
+    brick_bit(x, y, z, bsx, bsy, bsz, mask);
+    const int s = (__ldg(&slots[w]) >> (UP ? 4 : 0)) & 15;
+    if (s == kSelf) return w;
+    const int b = slot_bits(s), sg1 = slot_sign(s);
+    x += sg1 * (b & 1);
+    y += sg1 * ((b >> 1) & 1);
+    z += sg1 * (b >> 2);
+    w += sg1 * ((b & 1) + ((b >> 1) & 1) * G.nx + (b >> 2) * A);
+  }
+}
+
 // R5 / R6 (C3): for a join saddle s, m2 = <_h-largest minimum
 // reached from the h-lower link; for a split saddle, M2 = <_h-smallest
 // maximum from the h-upper link.  16 lanes per saddle, one per slot, each
@@ -549,33 +680,73 @@ __global__ void k_resolve(int2 *table, int n, Slabs S, int A, unsigned long long
 // Else h = g: if the pick differs from m1 (M1), mark m2 (join) or
 // M1 (split, amb-12).  Saddle lists, m1/M1 and labels are global ids; paths
 // leaving a slab are completed from the resolved boundary table; targets
-// outside the slab go to `remote` (sharded only).
-template <bool SPLIT, bool FROM_REF>
+// outside the slab go to `remote` (sharded only).  With a cache (tracking
+// mode) a saddle whose bricks saw no value or slot change since its cached
+// round re-emits its cached result instead of walking.
+template <bool SPLIT, bool FROM_REF, bool CACHE, bool SLAB>
 __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
                                                 const int32_t *__restrict__ sl, int n,
                                                 const uint8_t *__restrict__ slots,
                                                 const uint32_t *__restrict__ ref,
                                                 int32_t *ref_ext, uint32_t *marks, GridP G,
-                                                Slabs S, int32_t *remote,
+                                                Slabs S, int32_t *remote, EvCache EC, Track T,
                                                 unsigned long long *cnt) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = gt >> 4, l16 = threadIdx.x & 15;
   const bool active = k < n;
   const int A = G.nx * G.ny, off = G.zoff * A;
+  constexpr bool caching = !FROM_REF && CACHE;
+  int s = 0, sx = 0, sy = 0, sz = 0;
+  if (active) {
+    s = __ldg(&sl[k]) - off;  // local
+    sx = s % G.nx;
+    const int yz = s / G.nx;
+    sy = yz % G.ny;
+    sz = yz / G.ny;
+  }
+  const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
+  // ---- cached result still valid?  (the 16 lanes check the mask's bricks)
+  bool reuse = false;
+  uint16_t crnd = 0;
+  uint32_t cmask = 0;
+  if constexpr (caching) {
+   if (active) {
+    crnd = EC.rnd[k];
+    cmask = EC.mask[k];
+    reuse = crnd != 0 && !(cmask >> 31);
+    for (int j = l16; j < 27 && reuse; j += 16) {
+      if (!((cmask >> j) & 1u)) continue;
+      const int dz = j / 9 - 1, dy = (j / 3) % 3 - 1, dx = j % 3 - 1;
+      const int nb = (bsx + dx) + T.nbx * ((bsy + dy) + T.nby * (bsz + dz));
+      if (T.bval[nb] > crnd || T.bslot[nb] > crnd) reuse = false;
+    }
+   }
+  }
+  if constexpr (caching) {
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {  // every lane must take part in the shuffle
+      const int other = __shfl_xor_sync(0xffffffffu, (int)reuse, o);
+      reuse = reuse && other;
+    }
+  }
   int best = -1;
   float bv = 0.0f;
-  unsigned steps = 0;
-  if (active && l16 < kSlots) {
-    const int s = __ldg(&sl[k]) - off;  // local
-    const int x = s % G.nx, yz = s / G.nx, y = yz % G.ny, z = yz / G.ny;
-    const uint32_t valid = valid_mask(x, y, z, G);
+  uint32_t mask = 0;
+  if (active && !reuse && l16 < kSlots) {
+    const uint32_t valid = valid_mask(sx, sy, sz, G);
+    if (caching) brick_bit(sx, sy, sz, bsx, bsy, bsz, mask);
     if (valid & (1u << l16)) {
       const int u = s + G.delta[l16];
       const float hs = h[s], hu = h[u];
       const bool lower = (l16 < 7) ? (hu <= hs) : (hu < hs);
+      const int bb = slot_bits(l16), sg1 = slot_sign(l16);
+      const int ux = sx + sg1 * (bb & 1), uy = sy + sg1 * ((bb >> 1) & 1), uz = sz + sg1 * (bb >> 2);
+      if (caching) brick_bit(ux, uy, uz, bsx, bsy, bsz, mask);
       if (lower != SPLIT) {
-        const int e = walk<SPLIT, FROM_REF>(u, slots, ref, G, steps);
-        if (e >= 0) {
+        int e;
+        if constexpr (caching) e = walk_track<SPLIT>(u, ux, uy, uz, slots, G, bsx, bsy, bsz, mask);
+        else e = walk<SPLIT, FROM_REF, SLAB>(u, slots, ref, G);
+        if (!SLAB || e >= 0) {
           best = e + off;
           bv = h[e];
         } else {
@@ -596,23 +767,34 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
     else if (!SPLIT) take = (bv < ov) || (bv == ov && best < ob);  // SoS max
     else take = (ov < bv) || (ov == bv && ob < best);               // SoS min
     if (take) { best = ob; bv = ov; }
+    if constexpr (caching) mask |= __shfl_xor_sync(0xffffffffu, mask, o);
   }
   unsigned hit = 0;
   if (active && l16 == 0) {
     if (FROM_REF) {
       ref_ext[k] = best;
     } else {
-      const int want = ref_ext[k];
-      if (best >= 0 && best != want) {
-        const int t = (SPLIT ? want : best) - off;
-        if (t >= G.zb * A && t < G.ze * A) mark_vertex(marks, t, G);
-        else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = t + off;
+      int target = -1;
+      if (reuse) {
+        target = EC.tgt[k];
+      } else {
+        const int want = ref_ext[k];
+        if (best >= 0 && best != want) target = SPLIT ? want : best;
+        if (caching) {
+          EC.rnd[k] = (uint16_t)T.round;
+          EC.mask[k] = mask;
+          EC.tgt[k] = target;
+        }
+      }
+      if (target >= 0) {
+        const int t = target - off;
+        if (!SLAB || (t >= G.zb * A && t < G.ze * A)) mark_vertex(marks, t, G);
+        else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = target;
         hit = 1;
       }
     }
   }
   if (!FROM_REF) warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
-  if (!FROM_REF) warp_add(&cnt[C_WALK], steps);
 }
 
 // ------------------------------------------------ sharded helpers (z-slabs)
@@ -690,12 +872,13 @@ __device__ __forceinline__ void edit_vertex(float *__restrict__ g, uint8_t *__re
   ++ap;
 }
 
+template <bool TRACK>
 __global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
                                                     uint8_t *__restrict__ c,
                                                     uint32_t *__restrict__ marks,
                                                     const float *__restrict__ f, GridP G,
                                                     float xi, float delta, int N, int do_edit,
-                                                    unsigned long long *cnt) {
+                                                    Track T, unsigned long long *cnt) {
   const int lane = threadIdx.x & 31;
   const int64_t nwords = (int64_t)G.ny * G.ze * G.W;  // owned rows: [zb*ny, ze*ny)
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -714,10 +897,36 @@ __global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
         vt += __popc(word);
         marks[w] = 0u;
       }
+      const int64_t row = w / G.W;
+      const unsigned ap0 = ap;
       if (do_edit && ((word >> lane) & 1u)) {
-        const int64_t row = w / G.W;
         const int x = (int)(w - row * G.W) * 32 + lane;
         edit_vertex(g, c, f, (size_t)x + (size_t)G.nx * row, xi, delta, N, ap);
+      }
+      if (TRACK && (T.bval || T.act_next)) {
+        const uint32_t E = __ballot_sync(0xffffffffu, ap != ap0);  // edited lanes
+        if (E) {
+          const int wx = (int)(w - row * G.W), y = (int)(row % G.ny), z = (int)(row / G.ny);
+          if (T.bval && lane == 0)
+            T.bval[wx + T.nbx * ((y / BY) + T.nby * (z / BZ))] = (uint16_t)(T.round + 1);
+          if (T.act_next && lane < 7) {
+            // closed stars of the edited vertices: 7 (dz, dy) rows, x-1 / x+1
+            // spill into the neighbouring words
+            const int dz = lane < 2 ? -1 : (lane < 5 ? 0 : 1);
+            const int dy = (lane == 0 || lane == 2) ? -1 : ((lane == 4 || lane == 6) ? 1 : 0);
+            const bool neg = lane <= 3, pos = lane >= 3;  // x-1 for lanes 0..3, x+1 for 3..6
+            const int yy = y + dy, zz = z + dz;
+            if (yy >= 0 && yy < G.ny && zz >= 0 && zz < G.nz) {
+              uint32_t *r = T.act_next + (size_t)(yy + G.ny * zz) * G.W;
+              const int rem = G.nx - wx * 32;  // vertices of this row in the word
+              const uint32_t valid = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+              const uint32_t m = (E | (neg ? (E >> 1) : 0u) | (pos ? (E << 1) : 0u)) & valid;
+              atomicOr(&r[wx], m);
+              if (neg && (E & 1u) && wx > 0) atomicOr(&r[wx - 1], 0x80000000u);
+              if (pos && (E >> 31) && wx + 1 < G.W) atomicOr(&r[wx + 1], 1u);
+            }
+          }
+        }
       }
     }
   }

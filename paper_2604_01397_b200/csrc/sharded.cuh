@@ -420,9 +420,9 @@ struct ShardedRun {
   void events(Slab &x, const float *h, const int32_t *list, int n, int32_t *ext) {
     if (n <= 0) return;
     const int64_t threads = (int64_t)n * 16;
-    k_events<SPLIT, FROM_REF><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+    k_events<SPLIT, FROM_REF, false, true><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
         h, list, n, x.slots, x.ref, ext, x.marks, x.G, slabs_of(SPLIT ? x.tup : x.tdn), x.remote,
-        x.cnt);
+        EvCache{}, Track{}, x.cnt);
     CK(cudaGetLastError());
   }
 
@@ -437,7 +437,8 @@ struct ShardedRun {
     const bool c3 = !(flags & EXACTZ_NO_C3);
     zero_counters();
     each([&](Slab &x) {
-      k_stencil<<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.G, x.zc, x.cnt);
+      k_stencil<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.G, x.zc, Track{},
+                                                 x.cnt);
     });
     CK(cudaGetLastError());
     if (!(flags & EXACTZ_NO_C2) && nS > 1) {
@@ -517,8 +518,8 @@ struct ShardedRun {
       CK(cudaGetLastError());
     }
     each([&](Slab &x) {
-      k_count_edit<<<148 * 8, 256, 0, s>>>(x.g, x.c, x.marks, x.f, x.G, xi, delta, N,
-                                          do_edit ? 1 : 0, x.cnt);
+      k_count_edit<false><<<148 * 8, 256, 0, s>>>(x.g, x.c, x.marks, x.f, x.G, xi, delta, N,
+                                          do_edit ? 1 : 0, Track{}, x.cnt);
     });
     CK(cudaGetLastError());
     allreduce_counters();

@@ -169,3 +169,16 @@ def test_repeat_bit_identical(exactz):
     b = exactz.exactz_correct(f.cuda(), g.cuda(), xi)
     assert a.iters == b.iters
     assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
+
+
+@pytest.mark.parametrize("cfg,shape", [("C2", (40, 48, 200)), ("C3", (33, 40, 150)),
+                                       ("C4", (1, 300, 700))])
+def test_tracking_equals_dense(exactz, cfg, shape):
+    """Change tracking (active tiles + cached C3 results) gives the bits of
+    the dense passes, including every per-pass counter."""
+    f, g, xi = S.make(cfg, shape=shape, device="cuda")
+    a = exactz.exactz_correct(f, g, xi, stats_cap=100000)
+    b = exactz.exactz_correct(f, g, xi, flags=exactz.NO_TRACK, stats_cap=100000)
+    assert a.iters == b.iters and a.status == b.status
+    assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
+    assert a.stats == b.stats

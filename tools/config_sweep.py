@@ -14,7 +14,7 @@ for cfg in sys.argv[1:]:
     r = E.exactz_correct(f, g, xi, stats_cap=100000)  # warm
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
-    r = E.exactz_correct(f, g, xi, flags=E.PROFILE, stats_cap=100000)
+    r = E.exactz_correct(f, g, xi, flags=E.PROFILE | int(os.environ.get("FLAGS", "0"), 0), stats_cap=100000)
     s1.record(); torch.cuda.synchronize()
     ms = s0.elapsed_time(s1)
     V = f.numel()
