@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -261,21 +262,28 @@ struct Reference {
 template <bool SPLIT, bool FROM_REF>
 static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, const uint8_t *slots,
                           const uint32_t *ref, int32_t *ext, uint32_t *marks,
-                          EvCache ec = EvCache{}, Track tr = Track{}) {
+                          EvCache ec = EvCache{}, Track tr = Track{}, int *todo = nullptr,
+                          int *ntodo = nullptr) {
   if (n <= 0) return;
-  int64_t threads = (int64_t)n * 16;
+  const int64_t threads = (int64_t)n * 16;
   // algorithmic bytes: per saddle its id, its value, 14 link values, the
   // reached extrema's values and ids
-  C.run(FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS, 128ull * n, true, [&] {
-    const unsigned blocks = (unsigned)((threads + 255) / 256);
-    if (ec.rnd)
-      k_events<SPLIT, FROM_REF, true, false><<<blocks, 256, 0, C.s>>>(
-          h, sl, n, slots, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, ec, tr,
-          C.cnt);
-    else
-      k_events<SPLIT, FROM_REF, false, false><<<blocks, 256, 0, C.s>>>(
-          h, sl, n, slots, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, ec, tr,
-          C.cnt);
+  const int cls = FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS;
+  if (!ec.rnd) {
+    C.run(cls, 128ull * n, true, [&] {
+      k_events<SPLIT, FROM_REF, false><<<(unsigned)((threads + 255) / 256), 256, 0, C.s>>>(
+          h, sl, n, slots, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt);
+    });
+    return;
+  }
+  CK(cudaMemsetAsync(ntodo, 0, sizeof(int), C.s));
+  C.run(cls, 16ull * n, true, [&] {
+    k_events_check<SPLIT><<<(unsigned)((n + 255) / 256), 256, 0, C.s>>>(sl, n, ec, tr, marks,
+                                                                        C.G, todo, ntodo, C.cnt);
+  });
+  C.run(cls, 0, true, [&] {
+    k_events_cached<SPLIT><<<148 * 16, 256, 0, C.s>>>(h, sl, todo, ntodo, slots, ext, marks, C.G,
+                                                      ec, tr, C.cnt);
   });
 }
 
@@ -347,6 +355,7 @@ struct Tracking {
   int nbx = 0, nby = 0, nbz = 0, nb = 0;
   uint16_t *bval = nullptr, *bslot = nullptr;
   EvCache ecJ{}, ecP{};
+  int *todo = nullptr, *ntodo = nullptr;
   void geometry(const Ctx &C) {
     nbx = (C.G.nx + BX - 1) / BX;
     nby = (C.G.ny + BY - 1) / BY;
@@ -375,6 +384,8 @@ struct Tracking {
     };
     ecJ = cache(R.nJ);
     ecP = cache(R.nP);
+    todo = C.arena.get<int>(R.nJ > R.nP ? R.nJ : R.nP);
+    ntodo = C.arena.get<int>(1);
     cache_on = true;
   }
   Track track(int round) const {
@@ -430,9 +441,11 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
   if (c3) {
     const bool cache = trk && trk->cache_on;
     launch_events<false, false>(C, g, R.J, R.nJ, slots, R.ref, R.m1, marks,
-                                cache ? trk->ecJ : EvCache{}, T);
+                                cache ? trk->ecJ : EvCache{}, T, cache ? trk->todo : nullptr,
+                                cache ? trk->ntodo : nullptr);
     launch_events<true, false>(C, g, R.P, R.nP, slots, R.ref, R.M1, marks,
-                               cache ? trk->ecP : EvCache{}, T);
+                               cache ? trk->ecP : EvCache{}, T, cache ? trk->todo : nullptr,
+                               cache ? trk->ntodo : nullptr);
   }
   // bytes: mark words read (the per-edit 14 B are added once V_t is known)
   C.run(EXACTZ_K_EDIT, (uint64_t)C.V / 8, true, [&] {
@@ -510,6 +523,14 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   exactz_status st = EXACTZ_OK;
   Tracking trk;
   trk.geometry(C);
+  static const unsigned long long act_div = [] {
+    const char *e = std::getenv("EXACTZ_ACT_DIV");  // tuning knob (default 1024)
+    return e ? std::strtoull(e, nullptr, 10) : 1024ull;
+  }();
+  static const unsigned long long cache_div = [] {
+    const char *e = std::getenv("EXACTZ_CACHE_DIV");  // tuning knob (default 4)
+    return e ? std::strtoull(e, nullptr, 10) : 4ull;
+  }();
   unsigned long long prev_vt = (unsigned long long)V;
   const bool allow_track = !(flags & EXACTZ_NO_TRACK);
   for (;;) {
@@ -518,9 +539,9 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     if (allow_track && rows >= 1 && round < 65000) {
       // vertex activity once < 1/64 of the vertices are marked; the C3 cache
       // once the marks are sparse at brick scale
-      if (!(flags & 0x10u) && !trk.act_on && prev_vt * 64 <= (unsigned long long)V)
+      if (!(flags & 0x10u) && !trk.act_on && prev_vt * act_div <= (unsigned long long)V)
         trk.start_act(C);
-      if (!(flags & 0x20u) && !trk.cache_on && prev_vt * 32 <= (unsigned long long)trk.nb)
+      if (!(flags & 0x20u) && !trk.cache_on && prev_vt * cache_div <= (unsigned long long)trk.nb)
         trk.start_cache(C, R);
     }
     const bool tracked = allow_track && round < 65000 && (trk.act_on || trk.cache_on);

@@ -501,11 +501,15 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
   const int64_t w0 = (int64_t)G.ny * G.zb * G.W, nwords = (int64_t)G.ny * G.ze * G.W;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned n1 = 0, n2 = 0, n3 = 0;
-  for (int64_t w = w0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w < nwords;
-       w += nwarps) {
-    const uint32_t word = act[w];
-    if (!word) continue;
-    if (lane == 0) act[w] = 0u;
+  for (int64_t base = w0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
+       base < nwords; base += nwarps * 32) {
+   // 32 words per warp step, one per lane; only the non-zero ones are visited
+   const uint32_t mine = (base + lane < nwords) ? act[base + lane] : 0u;
+   if (mine) act[base + lane] = 0u;  // consumed
+   for (uint32_t nzw = __ballot_sync(0xffffffffu, mine != 0u); nzw; nzw &= nzw - 1) {
+    const int j = __ffs(nzw) - 1;
+    const uint32_t word = __shfl_sync(0xffffffffu, mine, j);
+    const int64_t w = base + j;
     const int row = (int)(w / G.W), wx = (int)(w - (int64_t)row * G.W);
     const int y = row % G.ny, z = row / G.ny, x = wx * 32 + lane;
     uint32_t tgt = 0;
@@ -545,6 +549,7 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
       const unsigned fired = __ballot_sync(0xffffffffu, tgt != 0);
       if (lane == 0 && fired) atomicOr(&T.act_next[w], fired);
     }
+   }
   }
   warp_add(&cnt[C_N1 + 0], n1);
   warp_add(&cnt[C_N1 + 1], n2);
@@ -680,22 +685,17 @@ __device__ __forceinline__ int walk_track(int u, int x, int y, int z,
 // Else h = g: if the pick differs from m1 (M1), mark m2 (join) or
 // M1 (split, amb-12).  Saddle lists, m1/M1 and labels are global ids; paths
 // leaving a slab are completed from the resolved boundary table; targets
-// outside the slab go to `remote` (sharded only).  With a cache (tracking
-// mode) a saddle whose bricks saw no value or slot change since its cached
-// round re-emits its cached result instead of walking.
+// outside the slab go to `remote` (sharded only).  CACHE: the result, with
+// the bricks the saddle depends on, is stored for k_events_check.
 template <bool SPLIT, bool FROM_REF, bool CACHE, bool SLAB>
-__global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
-                                                const int32_t *__restrict__ sl, int n,
-                                                const uint8_t *__restrict__ slots,
-                                                const uint32_t *__restrict__ ref,
-                                                int32_t *ref_ext, uint32_t *marks, GridP G,
-                                                Slabs S, int32_t *remote, EvCache EC, Track T,
-                                                unsigned long long *cnt) {
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int k = gt >> 4, l16 = threadIdx.x & 15;
-  const bool active = k < n;
+__device__ __forceinline__ unsigned events_group(
+    int k, bool active, const float *__restrict__ h, const int32_t *__restrict__ sl,
+    const uint8_t *__restrict__ slots, const uint32_t *__restrict__ ref, int32_t *ref_ext,
+    uint32_t *marks, const GridP &G, const Slabs &S, int32_t *remote, const EvCache &EC,
+    const Track &T, unsigned long long *cnt) {
+  const int l16 = threadIdx.x & 15;
+  const unsigned gmask = 0xffffu << (threadIdx.x & 16);  // this 16-lane group
   const int A = G.nx * G.ny, off = G.zoff * A;
-  constexpr bool caching = !FROM_REF && CACHE;
   int s = 0, sx = 0, sy = 0, sz = 0;
   if (active) {
     s = __ldg(&sl[k]) - off;  // local
@@ -705,46 +705,23 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
     sz = yz / G.ny;
   }
   const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
-  // ---- cached result still valid?  (the 16 lanes check the mask's bricks)
-  bool reuse = false;
-  uint16_t crnd = 0;
-  uint32_t cmask = 0;
-  if constexpr (caching) {
-   if (active) {
-    crnd = EC.rnd[k];
-    cmask = EC.mask[k];
-    reuse = crnd != 0 && !(cmask >> 31);
-    for (int j = l16; j < 27 && reuse; j += 16) {
-      if (!((cmask >> j) & 1u)) continue;
-      const int dz = j / 9 - 1, dy = (j / 3) % 3 - 1, dx = j % 3 - 1;
-      const int nb = (bsx + dx) + T.nbx * ((bsy + dy) + T.nby * (bsz + dz));
-      if (T.bval[nb] > crnd || T.bslot[nb] > crnd) reuse = false;
-    }
-   }
-  }
-  if constexpr (caching) {
-#pragma unroll
-    for (int o = 8; o >= 1; o >>= 1) {  // every lane must take part in the shuffle
-      const int other = __shfl_xor_sync(0xffffffffu, (int)reuse, o);
-      reuse = reuse && other;
-    }
-  }
   int best = -1;
   float bv = 0.0f;
   uint32_t mask = 0;
-  if (active && !reuse && l16 < kSlots) {
+  if (active && l16 < kSlots) {
     const uint32_t valid = valid_mask(sx, sy, sz, G);
-    if (caching) brick_bit(sx, sy, sz, bsx, bsy, bsz, mask);
+    if (CACHE) brick_bit(sx, sy, sz, bsx, bsy, bsz, mask);
     if (valid & (1u << l16)) {
       const int u = s + G.delta[l16];
       const float hs = h[s], hu = h[u];
       const bool lower = (l16 < 7) ? (hu <= hs) : (hu < hs);
       const int bb = slot_bits(l16), sg1 = slot_sign(l16);
-      const int ux = sx + sg1 * (bb & 1), uy = sy + sg1 * ((bb >> 1) & 1), uz = sz + sg1 * (bb >> 2);
-      if (caching) brick_bit(ux, uy, uz, bsx, bsy, bsz, mask);
+      const int ux = sx + sg1 * (bb & 1), uy = sy + sg1 * ((bb >> 1) & 1),
+                uz = sz + sg1 * (bb >> 2);
+      if (CACHE) brick_bit(ux, uy, uz, bsx, bsy, bsz, mask);
       if (lower != SPLIT) {
         int e;
-        if constexpr (caching) e = walk_track<SPLIT>(u, ux, uy, uz, slots, G, bsx, bsy, bsz, mask);
+        if constexpr (CACHE) e = walk_track<SPLIT>(u, ux, uy, uz, slots, G, bsx, bsy, bsz, mask);
         else e = walk<SPLIT, FROM_REF, SLAB>(u, slots, ref, G);
         if (!SLAB || e >= 0) {
           best = e + off;
@@ -759,15 +736,15 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
   }
 #pragma unroll
   for (int o = 8; o >= 1; o >>= 1) {
-    int ob = __shfl_xor_sync(0xffffffffu, best, o);
-    float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    int ob = __shfl_xor_sync(gmask, best, o);
+    float ov = __shfl_xor_sync(gmask, bv, o);
     bool take;
     if (ob < 0) take = false;
     else if (best < 0) take = true;
     else if (!SPLIT) take = (bv < ov) || (bv == ov && best < ob);  // SoS max
     else take = (ov < bv) || (ov == bv && ob < best);               // SoS min
     if (take) { best = ob; bv = ov; }
-    if constexpr (caching) mask |= __shfl_xor_sync(0xffffffffu, mask, o);
+    if (CACHE) mask |= __shfl_xor_sync(gmask, mask, o);
   }
   unsigned hit = 0;
   if (active && l16 == 0) {
@@ -775,16 +752,12 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
       ref_ext[k] = best;
     } else {
       int target = -1;
-      if (reuse) {
-        target = EC.tgt[k];
-      } else {
-        const int want = ref_ext[k];
-        if (best >= 0 && best != want) target = SPLIT ? want : best;
-        if (caching) {
-          EC.rnd[k] = (uint16_t)T.round;
-          EC.mask[k] = mask;
-          EC.tgt[k] = target;
-        }
+      const int want = ref_ext[k];
+      if (best >= 0 && best != want) target = SPLIT ? want : best;
+      if (CACHE) {
+        EC.rnd[k] = (uint16_t)T.round;
+        EC.mask[k] = mask;
+        EC.tgt[k] = target;
       }
       if (target >= 0) {
         const int t = target - off;
@@ -794,7 +767,94 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
       }
     }
   }
+  return hit;
+}
+
+// one 16-lane group per saddle of sl[0..n)
+template <bool SPLIT, bool FROM_REF, bool SLAB>
+__global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
+                                                const int32_t *__restrict__ sl, int n,
+                                                const uint8_t *__restrict__ slots,
+                                                const uint32_t *__restrict__ ref,
+                                                int32_t *ref_ext, uint32_t *marks, GridP G,
+                                                Slabs S, int32_t *remote,
+                                                unsigned long long *cnt) {
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+  const unsigned hit = events_group<SPLIT, FROM_REF, false, SLAB>(
+      k, k < n, h, sl, slots, ref, ref_ext, marks, G, S, remote, EvCache{}, Track{}, cnt);
   if (!FROM_REF) warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
+}
+
+// Tracking: a saddle whose cached result is still valid (no brick it depends
+// on changed since the cached pass) re-emits it; the others are listed for
+// k_events_cached.  One thread per saddle.
+template <bool SPLIT>
+__global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict__ sl, int n,
+                                                      EvCache EC, Track T, uint32_t *marks,
+                                                      GridP G, int *todo, int *ntodo,
+                                                      unsigned long long *cnt) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  bool valid = false;
+  unsigned hit = 0;
+  if (k < n) {
+    const uint16_t rnd = EC.rnd[k];
+    const uint32_t mask = EC.mask[k];
+    valid = rnd != 0 && !(mask >> 31);
+    if (valid) {
+      const int s = sl[k];
+      const int sx = s % G.nx, yz = s / G.nx, sy = yz % G.ny, sz = yz / G.ny;
+      const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
+      for (uint32_t m = mask; m && valid; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const int dz = j / 9 - 1, dy = (j / 3) % 3 - 1, dx = j % 3 - 1;
+        const int nb = (bsx + dx) + T.nbx * ((bsy + dy) + T.nby * (bsz + dz));
+        if (T.bval[nb] > rnd || T.bslot[nb] > rnd) valid = false;
+      }
+    }
+    if (valid) {
+      const int t = EC.tgt[k];
+      if (t >= 0) {
+        mark_vertex(marks, t, G);
+        hit = 1;
+      }
+    }
+  }
+  // warp-aggregated append of the saddles to recompute
+  const unsigned need = __ballot_sync(0xffffffffu, k < n && !valid);
+  if (need) {
+    const int lane = threadIdx.x & 31, leader = __ffs(need) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(ntodo, __popc(need));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if ((need >> lane) & 1u) todo[base + __popc(need & ((1u << lane) - 1u))] = k;
+  }
+  warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
+}
+
+// recompute (and cache) the listed saddles: warps stride over the list, two
+// 16-lane groups per warp
+template <bool SPLIT>
+__global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__ h,
+                                                       const int32_t *__restrict__ sl,
+                                                       const int *__restrict__ todo,
+                                                       const int *__restrict__ ntodo,
+                                                       const uint8_t *__restrict__ slots,
+                                                       int32_t *ref_ext, uint32_t *marks,
+                                                       GridP G, EvCache EC, Track T,
+                                                       unsigned long long *cnt) {
+  const int n = *ntodo;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned hit = 0;
+  for (int g0 = warp * 2; g0 < n; g0 += nwarps * 2) {
+    const int g = g0 + ((threadIdx.x >> 4) & 1);
+    const bool active = g < n;
+    const int k = active ? todo[g] : 0;
+    hit += events_group<SPLIT, false, true, false>(k, active, h, sl, slots, nullptr, ref_ext,
+                                                   marks, G, Slabs{nullptr, 1, nullptr},
+                                                   nullptr, EC, T, cnt);
+  }
+  warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
 }
 
 // ------------------------------------------------ sharded helpers (z-slabs)
@@ -884,19 +944,19 @@ __global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned vt = 0, ap = 0;
   for (int64_t w0 = (int64_t)G.ny * G.zb * G.W +
-                    (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4;
-       w0 < nwords; w0 += nwarps * 4) {
-    // lanes 0..3 fetch the 4 words of this batch; broadcast by shuffle
-    uint32_t mine = (lane < 4 && w0 + lane < nwords) ? marks[w0 + lane] : 0u;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint32_t word = __shfl_sync(0xffffffffu, mine, j);
-      if (!word) continue;
+                    (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
+       w0 < nwords; w0 += nwarps * 32) {
+    // 32 words per warp step (one per lane, coalesced); only non-zero words
+    // are visited, all lanes together
+    const uint32_t mine = (w0 + lane < nwords) ? marks[w0 + lane] : 0u;
+    if (mine) {
+      vt += __popc(mine);
+      marks[w0 + lane] = 0u;
+    }
+    for (uint32_t nzw = __ballot_sync(0xffffffffu, mine != 0u); nzw; nzw &= nzw - 1) {
+      const int j = __ffs(nzw) - 1;
+      const uint32_t word = __shfl_sync(0xffffffffu, mine, j);
       const int64_t w = w0 + j;
-      if (lane == 0) {
-        vt += __popc(word);
-        marks[w] = 0u;
-      }
       const int64_t row = w / G.W;
       const unsigned ap0 = ap;
       if (do_edit && ((word >> lane) & 1u)) {

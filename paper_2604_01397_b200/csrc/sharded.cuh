@@ -420,9 +420,9 @@ struct ShardedRun {
   void events(Slab &x, const float *h, const int32_t *list, int n, int32_t *ext) {
     if (n <= 0) return;
     const int64_t threads = (int64_t)n * 16;
-    k_events<SPLIT, FROM_REF, false, true><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+    k_events<SPLIT, FROM_REF, true><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
         h, list, n, x.slots, x.ref, ext, x.marks, x.G, slabs_of(SPLIT ? x.tup : x.tdn), x.remote,
-        EvCache{}, Track{}, x.cnt);
+        x.cnt);
     CK(cudaGetLastError());
   }
 
