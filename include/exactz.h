@@ -74,6 +74,7 @@ enum {
   EXACTZ_K_EVENTS,       /* R5/R6 (C3) incl. the label walks (O6) */
   EXACTZ_K_EDIT,         /* count + bounded edits (O9) */
   EXACTZ_K_LABELS,       /* full label outputs (pointer jumping) */
+  EXACTZ_K_SPARSE,       /* sparse R1-R3 passes over the active vertices (tracking) */
   EXACTZ_K_CLASSES = 8
 };
 

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_PKG, "libexactz.so")
 OK, EINVAL, EBOUND, ESTUCK, EUNSUPPORTED, ECUDA, ENCCL, ENOMEM = 0, 2, 3, 4, 5, 6, 7, 8
 NO_C2, NO_C3, PROFILE, NO_TRACK = 0x1, 0x2, 0x4, 0x8
 KERNEL_CLASSES = ("validate", "reference", "stencil", "saddle_order", "events", "edit", "labels",
-                  "spare")
+                  "stencil_sparse")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g;"

@@ -265,7 +265,7 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
                           EvCache ec = EvCache{}, Track tr = Track{}, int *todo = nullptr,
                           int *ntodo = nullptr) {
   if (n <= 0) return;
-  const int64_t threads = (int64_t)n * 16;
+  const int64_t threads = (int64_t)n * 8;  // 8 lanes per saddle
   // algorithmic bytes: per saddle its id, its value, 14 link values, the
   // reached extrema's values and ids
   const int cls = FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS;
@@ -427,7 +427,7 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
                                                         C.cnt);
     });
   } else {
-    C.run(EXACTZ_K_STENCIL, (uint64_t)C.V / 8, true, [&] {
+    C.run(EXACTZ_K_SPARSE, (uint64_t)C.V / 8, true, [&] {
       k_stencil_sparse<<<148 * 8, 256, 0, C.s>>>(g, R.ref, marks, slots, trk->act[trk->cur],
                                                  C.G, T, C.cnt);
     });

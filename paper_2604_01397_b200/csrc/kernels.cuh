@@ -770,7 +770,128 @@ __device__ __forceinline__ unsigned events_group(
   return hit;
 }
 
-// one 16-lane group per saddle of sl[0..n)
+// Same rules with 8 lanes per saddle: lane l handles slots l and l + 8 and
+// walks both paths interleaved (two independent loads in flight per lane);
+// four saddles per warp halve the issue cost of the per-saddle work.
+template <bool UP, bool FROM_REF>
+__device__ __forceinline__ int next_slot(int w, const uint8_t *__restrict__ slots,
+                                         const uint32_t *__restrict__ ref) {
+  if (FROM_REF) return (__ldg(&ref[w]) >> (UP ? 18 : 14)) & 15;
+  return (__ldg(&slots[w]) >> (UP ? 4 : 0)) & 15;
+}
+
+template <bool SPLIT, bool FROM_REF, bool SLAB>
+__device__ __forceinline__ unsigned events_group8(
+    int k, bool active, const float *__restrict__ h, const int32_t *__restrict__ sl,
+    const uint8_t *__restrict__ slots, const uint32_t *__restrict__ ref, int32_t *ref_ext,
+    uint32_t *marks, const GridP &G, const Slabs &S, int32_t *remote, unsigned long long *cnt) {
+  const int l8 = threadIdx.x & 7;
+  const unsigned gmask = 0xffu << (threadIdx.x & 24);
+  const int A = G.nx * G.ny, off = G.zoff * A, lo = G.zb * A, hi = G.ze * A;
+  int best = -1;
+  float bv = 0.0f;
+  if (active) {
+    const int s = __ldg(&sl[k]) - off;  // local
+    const int sx = s % G.nx, yz = s / G.nx, sy = yz % G.ny, sz = yz / G.ny;
+    const uint32_t valid = valid_mask(sx, sy, sz, G);
+    const float hs = h[s];
+    int w[2];
+    bool go[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int slot = l8 + 8 * j;
+      go[j] = false;
+      w[j] = 0;
+      if (slot < kSlots && (valid & (1u << slot))) {
+        const int u = s + G.delta[slot];
+        const float hu = h[u];
+        const bool lower = (slot < 7) ? (hu <= hs) : (hu < hs);
+        if (lower != SPLIT) {
+          go[j] = true;
+          w[j] = u;
+        }
+      }
+    }
+    int e[2] = {0, 0};
+    bool ex[2] = {false, false};  // exits (sharded)
+    bool run[2] = {go[0], go[1]};
+    while (run[0] || run[1]) {
+      int sv[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        sv[j] = kSelf;
+        if (run[j]) {
+          if (SLAB && (w[j] < lo || w[j] >= hi)) {
+            ex[j] = true;
+            e[j] = w[j];
+            run[j] = false;
+          } else {
+            sv[j] = next_slot<SPLIT, FROM_REF>(w[j], slots, ref);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (!run[j]) continue;
+        if (sv[j] == kSelf) {
+          e[j] = w[j];
+          run[j] = false;
+        } else {
+          const int b = slot_bits(sv[j]);
+          w[j] += slot_sign(sv[j]) * ((b & 1) + ((b >> 1) & 1) * G.nx + (b >> 2) * A);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (!go[j]) continue;
+      int lab;
+      float val;
+      if (!SLAB || !ex[j]) {
+        lab = e[j] + off;
+        val = h[e[j]];
+      } else {
+        const int2 t = table_entry(S, e[j] + off, A);
+        lab = t.x;
+        val = __int_as_float(t.y);
+      }
+      bool take;
+      if (best < 0) take = true;
+      else if (!SPLIT) take = (bv < val) || (bv == val && best < lab);
+      else take = (val < bv) || (val == bv && lab < best);
+      if (take) { best = lab; bv = val; }
+    }
+  }
+#pragma unroll
+  for (int o = 4; o >= 1; o >>= 1) {
+    int ob = __shfl_xor_sync(gmask, best, o);
+    float ov = __shfl_xor_sync(gmask, bv, o);
+    bool take;
+    if (ob < 0) take = false;
+    else if (best < 0) take = true;
+    else if (!SPLIT) take = (bv < ov) || (bv == ov && best < ob);  // SoS max
+    else take = (ov < bv) || (ov == bv && ob < best);               // SoS min
+    if (take) { best = ob; bv = ov; }
+  }
+  unsigned hit = 0;
+  if (active && l8 == 0) {
+    if (FROM_REF) {
+      ref_ext[k] = best;
+    } else {
+      const int want = ref_ext[k];
+      if (best >= 0 && best != want) {
+        const int target = SPLIT ? want : best;
+        const int t = target - off;
+        if (!SLAB || (t >= G.zb * A && t < G.ze * A)) mark_vertex(marks, t, G);
+        else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = target;
+        hit = 1;
+      }
+    }
+  }
+  return hit;
+}
+
+// one 8-lane group per saddle of sl[0..n)
 template <bool SPLIT, bool FROM_REF, bool SLAB>
 __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
                                                 const int32_t *__restrict__ sl, int n,
@@ -779,9 +900,9 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
                                                 int32_t *ref_ext, uint32_t *marks, GridP G,
                                                 Slabs S, int32_t *remote,
                                                 unsigned long long *cnt) {
-  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
-  const unsigned hit = events_group<SPLIT, FROM_REF, false, SLAB>(
-      k, k < n, h, sl, slots, ref, ref_ext, marks, G, S, remote, EvCache{}, Track{}, cnt);
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const unsigned hit = events_group8<SPLIT, FROM_REF, SLAB>(k, k < n, h, sl, slots, ref, ref_ext,
+                                                            marks, G, S, remote, cnt);
   if (!FROM_REF) warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
 }
 

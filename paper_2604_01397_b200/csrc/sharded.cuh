@@ -419,7 +419,7 @@ struct ShardedRun {
   template <bool SPLIT, bool FROM_REF>
   void events(Slab &x, const float *h, const int32_t *list, int n, int32_t *ext) {
     if (n <= 0) return;
-    const int64_t threads = (int64_t)n * 16;
+    const int64_t threads = (int64_t)n * 8;
     k_events<SPLIT, FROM_REF, true><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
         h, list, n, x.slots, x.ref, ext, x.marks, x.G, slabs_of(SPLIT ? x.tup : x.tdn), x.remote,
         x.cnt);
