@@ -64,6 +64,10 @@ typedef enum {
                                (exactz_stats.kernel_ms); results are unchanged */
 #define EXACTZ_NO_TRACK 0x8u /* debug: dense passes only (no change tracking; results
                                 are identical) */
+#define EXACTZ_REFORMULATED 0x10u /* reformulated event constraints: the
+                                     f-order of ALL critical points is checked on
+                                     adjacent pairs (rule R7, counted in n[4]) instead
+                                     of the label-based C3 rules R5/R6 */
 
 /* kernel classes reported by EXACTZ_PROFILE */
 enum {
@@ -84,7 +88,8 @@ typedef struct {
   uint64_t applied;    /* edits applied this round (marked and not yet at f - xi) */
   uint64_t n[6];       /* per-rule counts: R1 max-neighbour, R2 min-neighbour,
                           R3 flipped (vertex, link-vertex) pairs at saddles / type
-                          changes, R4 flipped adjacent saddles, R5 join events,
+                          changes, R4 flipped adjacent saddles, R5 join events
+                          (R7 flipped adjacent critical points when REFORMULATED),
                           R6 split events */
   uint64_t walk_steps; /* reserved for diagnostics (0 in this build) */
 } exactz_iter_stats;

@@ -29,8 +29,9 @@
 #define ORC_ESTUCK 4
 #define ORC_ENOMEM 8
 
-#define ORC_NO_C2 1u /* debug: skip rule R4 (C2) */
-#define ORC_NO_C3 2u /* debug: skip rules R5/R6 (C3) */
+#define ORC_NO_C2 1u    /* debug: skip rule R4 (C2) */
+#define ORC_NO_C3 2u    /* debug: skip rules R5/R6 (C3) */
+#define ORC_REFORM 16u  /* reformulated event constraints: R7 instead of R5/R6 */
 
 #define CLS_REGULAR 0
 #define CLS_MIN 1
@@ -233,8 +234,9 @@ static void path_labels(int64_t V, const int32_t *ptr, int32_t *lab, int32_t *st
 typedef struct {
   uint8_t *nlc, *nuc, *cls;
   int32_t *up, *dn, *lab_dn, *lab_up;
-  int64_t nS, nJ, nP;
+  int64_t nS, nJ, nP, nC;
   int32_t *S, *J, *P, *m1, *M1; /* m1 indexed like J, M1 like P */
+  int32_t *CP;                  /* all critical points sorted by <_f (reformulation) */
 } Ref;
 
 static const float *sort_h; /* single-threaded qsort context */
@@ -247,7 +249,7 @@ static int cmp_sos_asc(const void *a, const void *b) {
 static void free_ref(Ref *R) {
   free(R->nlc); free(R->nuc); free(R->cls); free(R->up); free(R->dn);
   free(R->lab_dn); free(R->lab_up); free(R->S); free(R->J); free(R->P);
-  free(R->m1); free(R->M1);
+  free(R->m1); free(R->M1); free(R->CP);
   memset(R, 0, sizeof(*R));
 }
 
@@ -277,11 +279,24 @@ static int build_ref(const Grid *G, const float *f, Ref *R, int32_t *stack) {
   }
   path_labels(V, R->dn, R->lab_dn, stack);
   path_labels(V, R->up, R->lab_up, stack);
+  int64_t nC = 0;
+  for (int64_t i = 0; i < V; i++) nC += (R->cls[i] != CLS_REGULAR);
   R->S = malloc(4 * (nS + 1)); R->J = malloc(4 * (nJ + 1)); R->P = malloc(4 * (nP + 1));
-  R->m1 = malloc(4 * (nJ + 1)); R->M1 = malloc(4 * (nP + 1));
-  if (!R->S || !R->J || !R->P || !R->m1 || !R->M1) {
+  R->m1 = malloc(4 * (nJ + 1)); R->M1 = malloc(4 * (nP + 1)); R->CP = malloc(4 * (nC + 1));
+  if (!R->S || !R->J || !R->P || !R->m1 || !R->M1 || !R->CP) {
     free_ref(R);
     return ORC_ENOMEM;
+  }
+  /* Reformulation: "the reformulated event constraints preserve
+   * the ordering of all critical points" -- every non-regular vertex of f,
+   * sorted by <_f. */
+  R->nC = nC;
+  {
+    int64_t c = 0;
+    for (int64_t i = 0; i < V; i++)
+      if (R->cls[i] != CLS_REGULAR) R->CP[c++] = (int32_t)i;
+    sort_h = f;
+    qsort(R->CP, nC, 4, cmp_sos_asc);
   }
   R->nS = nS; R->nJ = nJ; R->nP = nP;
   int64_t s = 0;
@@ -396,9 +411,25 @@ static void detect(const Grid *G, const float *f, const Ref *R, const float *g, 
     }
   }
 
+  /* R7 (reformulated C3): "each iteration only requires
+   * exchanging the scalar value of each critical point with its immediate
+   * predecessor and successor (determined by the sorted sequence in the
+   * original data). Violations are detected by comparing the current
+   * ordering with the original one ... and corrected by applying edits to
+   * restore the correct order": adjacent a = CP[k] <_f b = CP[k+1]; if
+   * b <_g a, decrease a (the f-smaller, as for C2).  Counted in cnt[5]. */
+  if (!(flags & ORC_NO_C3) && (flags & ORC_REFORM)) {
+    for (int64_t k = 0; k + 1 < R->nC; k++) {
+      int32_t a = R->CP[k], b = R->CP[k + 1];
+      if (sos_less(g, b, a)) {
+        mark[a] = 1;
+        cnt[5]++;
+      }
+    }
+  }
   /* R5/R6 (C3; amb-11, amb-12): the extremum EGP selects for each
    * saddle, evaluated on the extremum graph of g (labels of g). */
-  if (!(flags & ORC_NO_C3)) {
+  if (!(flags & ORC_NO_C3) && !(flags & ORC_REFORM)) {
     path_labels(V, W->dng, W->labdn, W->stack);
     path_labels(V, W->upg, W->labup, W->stack);
     for (int64_t k = 0; k < R->nJ; k++) {

@@ -21,7 +21,7 @@ SRC = os.path.join(HERE, "exactz_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
 
 OK, EINVAL, EBOUND, ESTUCK, ENOMEM = 0, 2, 3, 4, 8
-NO_C2, NO_C3 = 1, 2
+NO_C2, NO_C3, REFORM = 1, 2, 16
 CLS_REGULAR, CLS_MIN, CLS_MAX, CLS_SADDLE = 0, 1, 2, 3
 
 

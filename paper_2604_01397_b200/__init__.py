@@ -16,7 +16,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libexactz.so")
 
 OK, EINVAL, EBOUND, ESTUCK, EUNSUPPORTED, ECUDA, ENCCL, ENOMEM = 0, 2, 3, 4, 5, 6, 7, 8
-NO_C2, NO_C3, PROFILE, NO_TRACK = 0x1, 0x2, 0x4, 0x8
+NO_C2, NO_C3, PROFILE, NO_TRACK, REFORMULATED = 0x1, 0x2, 0x4, 0x8, 0x10
 KERNEL_CLASSES = ("validate", "reference", "stencil", "saddle_order", "events", "edit", "labels",
                   "stencil_sparse")
 

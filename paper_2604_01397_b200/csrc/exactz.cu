@@ -257,7 +257,24 @@ struct Reference {
   uint32_t *ref = nullptr;
   int32_t *S = nullptr, *J = nullptr, *P = nullptr, *m1 = nullptr, *M1 = nullptr;
   int nS = 0, nJ = 0, nP = 0;
+  int32_t *CP = nullptr;  // reformulation: all critical points sorted by (f, idx)
+  int nC = 0;
 };
+
+// Sort 64-bit SoS keys (ordered(f) << 32 | idx) and keep the indices.
+static void sort_ids(Ctx &C, uint64_t *keys, int n, int32_t *ids) {
+  if (n <= 0) return;
+  uint64_t *sorted = C.arena.get<uint64_t>(n);
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, n, 0, 64, C.s));
+  void *tmp = C.arena.get<uint8_t>(tb);
+  C.run(EXACTZ_K_REFERENCE, 32ull * n, false, [&] {
+    CK(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, n, 0, 64, C.s));
+  });
+  C.run(EXACTZ_K_REFERENCE, 12ull * n, true, [&] {
+    k_keys_to_ids<<<blocks_for(n, 256, 1 << 30), 256, 0, C.s>>>(sorted, ids, n);
+  });
+}
 
 template <bool SPLIT, bool FROM_REF>
 static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, const uint8_t *slots,
@@ -288,15 +305,22 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
 }
 
 // O7: reference topology of f, computed once per call.
-static void build_reference(Ctx &C, const float *f, Reference &R) {
+static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = false) {
   int64_t V = C.V;
   R.ref = C.arena.get<uint32_t>(V);
   uint64_t *keys = C.arena.get<uint64_t>(V);
+  uint64_t *cpkeys = reform ? C.arena.get<uint64_t>(V) : nullptr;
   C.zero();
-  C.run(EXACTZ_K_REFERENCE, 8 * (uint64_t)V, true,
-        [&] { k_reference<<<C.rgrid, C.vblock, 0, C.s>>>(f, C.G, R.ref, keys, C.cnt); });
+  C.run(EXACTZ_K_REFERENCE, 8 * (uint64_t)V, true, [&] {
+    k_reference<<<C.rgrid, C.vblock, 0, C.s>>>(f, C.G, R.ref, keys, cpkeys, C.cnt);
+  });
   C.read();
   R.nS = (int)C.hcnt[C_NSADDLE];
+  if (reform) {  // the sorted sequence of all critical points of f
+    R.nC = (int)C.hcnt[C_NCP];
+    R.CP = C.arena.get<int32_t>(R.nC);
+    sort_ids(C, cpkeys, R.nC, R.CP);
+  }
   // S: all saddles sorted by the SoS key of f.  J, P: join / split
   // saddles in index (spatial) order, so that consecutive event checks walk
   // nearby integral paths (L1/L2 reuse); their order is otherwise irrelevant.
@@ -334,8 +358,10 @@ static void build_reference(Ctx &C, const float *f, Reference &R) {
   R.m1 = C.arena.get<int32_t>(R.nJ);
   R.M1 = C.arena.get<int32_t>(R.nP);
   // m1 / M1 by walking f's steepest paths from each saddle's link
-  launch_events<false, true>(C, f, R.J, R.nJ, nullptr, R.ref, R.m1, nullptr);
-  launch_events<true, true>(C, f, R.P, R.nP, nullptr, R.ref, R.M1, nullptr);
+  if (!reform) {
+    launch_events<false, true>(C, f, R.J, R.nJ, nullptr, R.ref, R.m1, nullptr);
+    launch_events<true, true>(C, f, R.P, R.nP, nullptr, R.ref, R.M1, nullptr);
+  }
 }
 
 struct PassOut {
@@ -438,7 +464,13 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
                                                                       C.cnt);
     });
   }
-  if (c3) {
+  if (c3 && (flags & EXACTZ_REFORMULATED) && R.nC > 1) {
+    // R7: adjacent critical points in the f order
+    C.run(EXACTZ_K_EVENTS, 8ull * R.nC, true, [&] {
+      k_saddle_order<<<blocks_for(R.nC, 256, 1 << 30), 256, 0, C.s>>>(g, R.CP, R.nC, marks, C.G,
+                                                                      C.cnt, C_N1 + 4);
+    });
+  } else if (c3 && !(flags & EXACTZ_REFORMULATED)) {
     const bool cache = trk && trk->cache_on;
     launch_events<false, false>(C, g, R.J, R.nJ, slots, R.ref, R.m1, marks,
                                 cache ? trk->ecJ : EvCache{}, T, cache ? trk->todo : nullptr,
@@ -510,7 +542,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   validate_inputs(C, f, g_in, eps);
   if (out != g_in) CK(cudaMemcpyAsync(out, g_in, V * sizeof(float), cudaMemcpyDeviceToDevice, s));
   Reference R;
-  build_reference(C, f, R);
+  build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
   uint8_t *c = (opts && opts->edit_counts) ? opts->edit_counts : C.arena.get<uint8_t>(V);
   uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
   uint8_t *slots = C.arena.get<uint8_t>(V);
@@ -539,9 +571,10 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     if (allow_track && rows >= 1 && round < 65000) {
       // vertex activity once < 1/64 of the vertices are marked; the C3 cache
       // once the marks are sparse at brick scale
-      if (!(flags & 0x10u) && !trk.act_on && prev_vt * act_div <= (unsigned long long)V)
+      if (!(flags & 0x100u) && !trk.act_on && prev_vt * act_div <= (unsigned long long)V)
         trk.start_act(C);
-      if (!(flags & 0x20u) && !trk.cache_on && prev_vt * cache_div <= (unsigned long long)trk.nb)
+      if (!(flags & (0x200u | EXACTZ_REFORMULATED)) && !trk.cache_on &&
+          prev_vt * cache_div <= (unsigned long long)trk.nb)
         trk.start_cache(C, R);
     }
     const bool tracked = allow_track && round < 65000 && (trk.act_on || trk.cache_on);
@@ -668,7 +701,7 @@ exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3]
     C.init(dims);
     validate_inputs(C, f, g, eps_abs);
     Reference R;
-    build_reference(C, f, R);
+    build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
     uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
     uint8_t *slots = C.arena.get<uint8_t>(V);
     CK(cudaMemsetAsync(marks, 0, C.mark_words() * sizeof(uint32_t), s));

@@ -42,6 +42,7 @@ enum Counter {
   C_KEYMAX = 13,
   C_NREMOTE = 14,  // sharded: remote marks appended by k_events
   C_WALK = 15,     // diagnostic: steps taken by the label walks of a pass
+  C_NCP = 8,       // reference: critical points (shares the slot of C_CHANGED)
   C_NCOUNTERS = 16
 };
 
@@ -232,8 +233,8 @@ __global__ void k_validate(const float *__restrict__ f, const float *__restrict_
 // SoS keys of the saddles are appended (sorted later).
 __device__ __forceinline__ void reference_vertex(const float *__restrict__ f, const GridP &G,
                                                  uint32_t *__restrict__ ref,
-                                                 uint64_t *saddle_keys, unsigned long long *cnt,
-                                                 int x, int y, int z) {
+                                                 uint64_t *saddle_keys, uint64_t *cp_keys,
+                                                 unsigned long long *cnt, int x, int y, int z) {
   int i = x + G.nx * (y + G.ny * z);
   uint32_t valid = valid_mask(x, y, z, G);
   Star st = eval_star(f, i, valid, G);
@@ -245,21 +246,25 @@ __device__ __forceinline__ void reference_vertex(const float *__restrict__ f, co
   ref[i] = st.lower | ((uint32_t)st.dn << 14) | ((uint32_t)st.up << 18) | ((uint32_t)nlc << 22) |
            ((uint32_t)nuc << 25) | ((uint32_t)sad << 28) | ((uint32_t)join << 29) |
            ((uint32_t)split << 30);
+  const uint32_t ig = (uint32_t)(i + G.zoff * G.nx * G.ny);  // global index (SoS)
   if (sad) {
     unsigned long long k = atomicAdd(&cnt[C_NSADDLE], 1ull);
-    const uint32_t ig = (uint32_t)(i + G.zoff * G.nx * G.ny);  // global index (SoS)
     saddle_keys[k] = ((uint64_t)ordered_key(f[i]) << 32) | ig;
+  }
+  if (cp_keys && (sad || isext)) {  // every critical point (reformulation)
+    unsigned long long k = atomicAdd(&cnt[C_NCP], 1ull);
+    cp_keys[k] = ((uint64_t)ordered_key(f[i]) << 32) | ig;
   }
 }
 
 // Persistent 2D grid over rows (y + ny*z) and x.
 __global__ void __launch_bounds__(128) k_reference(const float *__restrict__ f, GridP G,
                                                    uint32_t *__restrict__ ref,
-                                                   uint64_t *saddle_keys,
+                                                   uint64_t *saddle_keys, uint64_t *cp_keys,
                                                    unsigned long long *cnt) {
   for (int row = G.zb * G.ny + blockIdx.y; row < G.ze * G.ny; row += gridDim.y)
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < G.nx; x += gridDim.x * blockDim.x)
-      reference_vertex(f, G, ref, saddle_keys, cnt, x, row % G.ny, row / G.ny);
+      reference_vertex(f, G, ref, saddle_keys, cp_keys, cnt, x, row % G.ny, row / G.ny);
 }
 
 __global__ void k_keys_to_ids(const uint64_t *__restrict__ keys, int32_t *ids, int n) {
@@ -558,8 +563,11 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
 
 // R4 (C2): adjacent saddles a = S[k] <_f b = S[k+1]; if b <_g a,
 // decrease a (the f-smaller).
+// (also R7 of the reformulation over the list of all critical points, counted
+// in counter `ci`)
 __global__ void k_saddle_order(const float *__restrict__ g, const int32_t *__restrict__ S,
-                               int nS, uint32_t *marks, GridP G, unsigned long long *cnt) {
+                               int nS, uint32_t *marks, GridP G, unsigned long long *cnt,
+                               int ci = C_N1 + 3) {
   unsigned n4 = 0;
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k + 1 < nS) {
@@ -569,7 +577,7 @@ __global__ void k_saddle_order(const float *__restrict__ g, const int32_t *__res
       n4 = 1;
     }
   }
-  warp_add(&cnt[C_N1 + 3], n4);
+  warp_add(&cnt[ci], n4);
 }
 
 // Terminus of the steepest path from u (O6): follow 4-bit slot pointers.
@@ -983,7 +991,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
 // the owner of S[k] checks the pair (S[k], S[k+1]).
 __global__ void k_saddle_order_slab(const uint32_t *__restrict__ gS,
                                     const int32_t *__restrict__ S, int nS, uint32_t *marks,
-                                    GridP G, unsigned long long *cnt) {
+                                    GridP G, unsigned long long *cnt, int ci = C_N1 + 3) {
   unsigned n4 = 0;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int A = G.nx * G.ny, off = G.zoff * A;
@@ -997,7 +1005,7 @@ __global__ void k_saddle_order_slab(const uint32_t *__restrict__ gS,
       }
     }
   }
-  warp_add(&cnt[C_N1 + 3], n4);
+  warp_add(&cnt[ci], n4);
 }
 
 // gS[k] = bits of g at S[k] for owned saddles, 0 elsewhere (max-all-reduced)

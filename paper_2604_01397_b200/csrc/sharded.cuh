@@ -166,6 +166,9 @@ struct Slab {
   int nJ = 0, nP = 0;
   int2 *tdn = nullptr, *tup = nullptr;  // gathered boundary tables (2 p A)
   uint32_t *gS = nullptr;
+  uint64_t *cpkeys = nullptr;
+  int32_t *CP = nullptr;  // reformulation: all critical points, replicated
+  uint32_t *gC = nullptr;
   int32_t *remote = nullptr, *allremote = nullptr;
   unsigned long long *cnt = nullptr, *hcnt = nullptr;  // device counters / host mirror
   unsigned long long *nrem = nullptr;                    // per-rank remote counts (p)
@@ -178,7 +181,8 @@ struct ShardedRun {
   cudaStream_t s;
   Arena &A;
   std::vector<Slab> &sl;
-  int p, nx, ny, nz, nS = 0;
+  int p, nx, ny, nz, nS = 0, nC = 0;
+  bool reform = false;
   int *d_start = nullptr;  // slab starts (device), p + 1 entries
   int N;
   float xi, delta;
@@ -189,6 +193,7 @@ struct ShardedRun {
       : T(t), s(st), A(a), sl(slabs), p(t.nranks()), nx(nx_), ny(ny_), nz(nz_), N(N_), xi(xi_),
         flags(flags_) {
     delta = xi / (float)N;
+    reform = (flags & EXACTZ_REFORMULATED) != 0;
   }
 
   template <class F>
@@ -264,6 +269,7 @@ struct ShardedRun {
       CK(cudaMallocHost(&x.hcnt, C_NCOUNTERS * 8));
       x.nrem = A.get<unsigned long long>(2 * p);
       x.keys = A.get<uint64_t>(x.nzl * P);
+      if (reform) x.cpkeys = A.get<uint64_t>(x.nzl * P);
       x.tdn = A.get<int2>(2 * p * P);
       x.tup = A.get<int2>(2 * p * P);
       // owned planes from the caller; ghost planes NaN until the halo exchange
@@ -298,7 +304,7 @@ struct ShardedRun {
     each([&](Slab &x) {
       unsigned bx = std::min(8u, (unsigned)((nx + 127) / 128));
       unsigned by = (unsigned)std::min<int64_t>((int64_t)x.nzl * ny, 148 * 16 / bx + 1);
-      k_reference<<<dim3(bx, by), 128, 0, s>>>(x.f, x.G, x.ref, x.keys, x.cnt);
+      k_reference<<<dim3(bx, by), 128, 0, s>>>(x.f, x.G, x.ref, x.keys, x.cpkeys, x.cnt);
     });
     CK(cudaGetLastError());
     read_counters();
@@ -366,12 +372,66 @@ struct ShardedRun {
       x.M1 = A.get<int32_t>(std::max(x.nP, 1));
     });
     CK(cudaGetLastError());
+    if (reform) {
+      gather_sorted(C_NCP, [](Slab &x) { return x.cpkeys; },
+                    [](Slab &x, int32_t *ids) { x.CP = ids; }, nC);
+      each([&](Slab &x) { x.gC = A.get<uint32_t>(std::max(nC, 1)); });
+      return;
+    }
     // m1 / M1 from f's paths, completed across slabs
     boundary_tables(true);
     each([&](Slab &x) {
       events<false, true>(x, x.f, x.J, x.nJ, x.m1);
       events<true, true>(x, x.f, x.P, x.nP, x.M1);
     });
+  }
+
+  // Gather every rank's keys (count in counter ci), sort identically on every
+  // rank, keep the global ids (the same list everywhere).
+  template <class GetKeys, class SetIds>
+  void gather_sorted(int ci, GetKeys keys_of, SetIds set_ids, int &total) {
+    std::vector<unsigned long long *> nb;
+    each([&](Slab &x) {
+      CK(cudaMemsetAsync(x.nrem, 0, 2 * p * 8, s));
+      CK(cudaMemcpyAsync(x.nrem + x.rank, x.cnt + ci, 8, cudaMemcpyDeviceToDevice, s));
+      nb.push_back(x.nrem);
+    });
+    T.allreduce_sum_u64(nb, p);
+    std::vector<unsigned long long> counts(p);
+    CK(cudaMemcpyAsync(counts.data(), sl[0].nrem, p * 8, cudaMemcpyDeviceToHost, s));
+    sync();
+    unsigned long long mx = 1;
+    total = 0;
+    for (int r = 0; r < p; ++r) {
+      total += (int)counts[r];
+      mx = std::max(mx, counts[r]);
+    }
+    std::vector<const void *> ks;
+    std::vector<void *> ka;
+    std::vector<uint64_t *> all;
+    each([&](Slab &x) {
+      uint64_t *pad = A.get<uint64_t>(mx);
+      CK(cudaMemsetAsync(pad, 0xff, mx * 8, s));
+      CK(cudaMemcpyAsync(pad, keys_of(x), counts[x.rank] * 8, cudaMemcpyDeviceToDevice, s));
+      uint64_t *a = A.get<uint64_t>(mx * p);
+      ks.push_back(pad);
+      ka.push_back(a);
+      all.push_back(a);
+    });
+    T.allgather(ks, ka, mx * 8);
+    int l = 0;
+    each([&](Slab &x) {
+      uint64_t *sorted = A.get<uint64_t>(mx * p);
+      int32_t *ids = A.get<int32_t>(std::max(total, 1));
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, all[l], sorted, (int)(mx * p), 0, 64, s));
+      void *tmp = A.get<uint8_t>(tb);
+      CK(cub::DeviceRadixSort::SortKeys(tmp, tb, all[l], sorted, (int)(mx * p), 0, 64, s));
+      if (total) k_keys_to_ids<<<(total + 255) / 256, 256, 0, s>>>(sorted, ids, total);
+      set_ids(x, ids);
+      ++l;
+    });
+    CK(cudaGetLastError());
   }
 
   Slabs slabs_of(const int2 *table) const { return Slabs{d_start, p, table}; }
@@ -453,7 +513,19 @@ struct ShardedRun {
       });
       CK(cudaGetLastError());
     }
-    if (c3) {
+    if (c3 && reform && nC > 1) {  // R7 on replicated critical-point values
+      std::vector<uint32_t *> b;
+      each([&](Slab &x) {
+        k_fill_gS<<<(nC + 255) / 256, 256, 0, s>>>(x.g, x.CP, nC, x.gC, x.G);
+        b.push_back(x.gC);
+      });
+      T.allreduce_max_u32(b, nC);
+      each([&](Slab &x) {
+        k_saddle_order_slab<<<(nC + 255) / 256, 256, 0, s>>>(x.gC, x.CP, nC, x.marks, x.G, x.cnt,
+                                                            C_N1 + 4);
+      });
+      CK(cudaGetLastError());
+    } else if (c3 && !reform) {
       boundary_tables(false);
       each([&](Slab &x) {
         events<false, false>(x, x.g, x.J, x.nJ, x.m1);

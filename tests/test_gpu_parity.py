@@ -182,3 +182,21 @@ def test_tracking_equals_dense(exactz, cfg, shape):
     assert a.iters == b.iters and a.status == b.status
     assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
     assert a.stats == b.stats
+
+
+@pytest.mark.parametrize("cfg,shape", [("C1", None), ("C2", (20, 24, 131)), ("C3", (17, 21, 150)),
+                                       ("C4", (1, 90, 300))])
+def test_parity_reformulated(exactz, oracle, cfg, shape):
+    """NEXT-1: reformulated event constraints, bit-exact with the
+    oracle's REFORM mode."""
+    f, g, xi = S.make(cfg, shape=shape)
+    assert_parity(*run_both(exactz, oracle, f, g, xi, flags=16))
+
+
+def test_tracking_equals_dense_reformulated(exactz):
+    f, g, xi = S.make("C2", shape=(40, 48, 200), device="cuda")
+    a = exactz.exactz_correct(f, g, xi, flags=exactz.REFORMULATED, stats_cap=100000)
+    b = exactz.exactz_correct(f, g, xi, flags=exactz.REFORMULATED | exactz.NO_TRACK,
+                              stats_cap=100000)
+    assert a.iters == b.iters and a.stats == b.stats
+    assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))

@@ -71,3 +71,9 @@ def test_slabs_errors(exactz):
     bad = g.clone()
     bad.view(-1)[7] = f.view(-1)[7] + 3 * xi
     assert E.status_of(E.exactz_correct_slabs, f.cuda(), bad.cuda(), xi, 2) == E.EBOUND
+
+
+@pytest.mark.parametrize("p", [2, 5])
+def test_slabs_reformulated(exactz, p):
+    f, g, xi = S.make("C3", shape=(15, 20, 40))
+    assert_same(*both(exactz, f, g, xi, p, flags=exactz.REFORMULATED))
