@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", default="exactz", choices=["exactz", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=64, help="edge of the oracle's crop")
+    ap.add_argument("--no-reformulated", action="store_true",
+                    help="skip the extra timing of the reformulated constraints (NEXT-1)")
     return ap.parse_args()
 
 
@@ -330,6 +332,32 @@ def main():
     e2e_ms = float(te.item())
     same = bool(torch.equal(oh.view(torch.int32), out.cpu().view(torch.int32)))
 
+    # ---------------- the reformulated constraints, same workload
+    reform = None
+    if not args.no_reformulated:
+        def rstep():
+            if sharded:
+                return E.exactz_correct_sharded(comm, f_run, g_run, dims, xi, out=out,
+                                                flags=E.REFORMULATED)
+            return E.exactz_correct(f_run, g_run, xi, out=out, flags=E.REFORMULATED)
+        rstep()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        r0e, r1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kr = max(1, min(args.steps, 3))
+        r0e.record(stream)
+        for _ in range(kr):
+            rr = rstep()
+        r1e.record(stream)
+        torch.cuda.synchronize()
+        tr = torch.tensor([r0e.elapsed_time(r1e) / kr], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(tr, op=dist.ReduceOp.MAX)
+        reform = {"value": 4.0 * V / (float(tr.item()) / 1e3) / 1e9, "unit": "GB/s",
+                  "ms_per_step": float(tr.item()), "iterations": rr.iters,
+                  "speedup_vs_original": ms_step / float(tr.item())}
+
     # ---------------- CPU baseline: the oracle on a bounded crop (rank 0, N = 1)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -364,6 +392,7 @@ def main():
                     else "exactz_correct_host (pinned host buffers, copies inside the C call)",
                     "ms_per_step": e2e_ms, "bit_equal_to_device_run": same},
             "gpu_launches": launches,
+            "reformulated": reform,
             "clocks": ck,
             "version": E.version(),
         }

@@ -378,8 +378,8 @@ struct Tracking {
   int cur = 0;
   // C3 cache with brick stamps
   bool cache_on = false;
-  int nbx = 0, nby = 0, nbz = 0, nb = 0;
-  uint16_t *bval = nullptr, *bslot = nullptr;
+  int nbx = 0, nby = 0, nbz = 0, nb = 0, nsx = 0, nsy = 0, nsz = 0, nsb = 0;
+  uint16_t *bval = nullptr, *bslot = nullptr, *sbval = nullptr, *sbslot = nullptr;
   EvCache ecJ{}, ecP{};
   int *todo = nullptr, *ntodo = nullptr;
   void geometry(const Ctx &C) {
@@ -387,6 +387,10 @@ struct Tracking {
     nby = (C.G.ny + BY - 1) / BY;
     nbz = (C.G.nz + BZ - 1) / BZ;
     nb = nbx * nby * nbz;
+    nsx = (nbx + SB - 1) / SB;
+    nsy = (nby + SB - 1) / SB;
+    nsz = (nbz + SB - 1) / SB;
+    nsb = nsx * nsy * nsz;
   }
   void start_act(Ctx &C) {
     for (int k = 0; k < 2; ++k) {
@@ -396,14 +400,16 @@ struct Tracking {
     act_on = true;
   }
   void start_cache(Ctx &C, const Reference &R) {
-    uint16_t *st = C.arena.get<uint16_t>(2 * (size_t)nb);
-    CK(cudaMemsetAsync(st, 0, 2 * (size_t)nb * 2, C.s));
+    uint16_t *st = C.arena.get<uint16_t>(2 * (size_t)(nb + nsb));
+    CK(cudaMemsetAsync(st, 0, 2 * (size_t)(nb + nsb) * 2, C.s));
     bval = st;
     bslot = st + nb;
+    sbval = st + 2 * (size_t)nb;
+    sbslot = sbval + nsb;
     auto cache = [&](int n) {
       EvCache e;
       e.rnd = C.arena.get<uint16_t>(n);
-      e.mask = C.arena.get<uint32_t>(n);
+      e.mask = C.arena.get<unsigned long long>(n);
       e.tgt = C.arena.get<int32_t>(n);
       CK(cudaMemsetAsync(e.rnd, 0, (size_t)(n ? n : 1) * 2, C.s));
       return e;
@@ -420,9 +426,13 @@ struct Tracking {
     T.nby = nby;
     T.nbz = nbz;
     T.round = round;
+    T.nsx = nsx;
+    T.nsy = nsy;
     if (cache_on) {
       T.bval = bval;
       T.bslot = bslot;
+      T.sbval = sbval;
+      T.sbslot = sbslot;
     }
     if (act_on) T.act_next = act[cur ^ 1];
     return T;

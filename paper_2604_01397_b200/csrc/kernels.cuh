@@ -71,11 +71,20 @@ struct GridP {
 //    a saddle's cached C3 result is reused while no brick its walks touched
 //    changed.
 constexpr int BX = 32, BY = 8, BZ = 8;
+constexpr int SB = 4;  // superbrick = 4 x 4 x 4 bricks (128 x 32 x 32 vertices)
 struct Track {
   uint16_t *bval, *bslot;       // brick stamps (nullptr: C3 cache off)
+  uint16_t *sbval, *sbslot;     // superbrick stamps (max over its bricks)
   uint32_t *act_next;           // vertex activity for the next pass (nullptr: off)
   int nbx, nby, nbz, round;
+  int nsx, nsy;                 // superbrick grid (x, y extents)
 };
+
+__device__ __forceinline__ void stamp(uint16_t *b, uint16_t *sb, const Track &T, int bx, int by,
+                                      int bz, uint16_t v) {
+  b[bx + T.nbx * (by + T.nby * bz)] = v;
+  sb[bx / SB + T.nsx * (by / SB + T.nsy * (bz / SB))] = v;
+}
 
 // ref word layout (one uint32 per vertex, computed once from f):
 //   bits  0-13  f-lower mask (slot s set <=> neighbour s <_f i)
@@ -443,7 +452,7 @@ __global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
     }
     if (TRACK && T.bval) {  // slot-change stamp of this warp's brick
       const unsigned chg = __ballot_sync(0xffffffffu, schg);
-      if (tx == 0 && chg) T.bslot[bx + T.nbx * ((y / BY) + T.nby * (z / BZ))] = (uint16_t)T.round;
+      if (tx == 0 && chg) stamp(T.bslot, T.sbslot, T, bx, y / BY, z / BZ, (uint16_t)T.round);
       schg = false;
     }
     if (TRACK && T.act_next) {  // fired vertices stay active next pass
@@ -548,7 +557,7 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
     }
     if (T.bval) {
       const unsigned chg = __ballot_sync(0xffffffffu, schg);
-      if (lane == 0 && chg) T.bslot[wx + T.nbx * ((y / BY) + T.nby * (z / BZ))] = (uint16_t)T.round;
+      if (lane == 0 && chg) stamp(T.bslot, T.sbslot, T, wx, y / BY, z / BZ, (uint16_t)T.round);
     }
     if (T.act_next) {
       const unsigned fired = __ballot_sync(0xffffffffu, tgt != 0);
@@ -655,22 +664,34 @@ __global__ void k_resolve(int2 *table, int n, Slabs S, int A, unsigned long long
 // neighbourhood (never reused); tgt = the marked target or -1.
 struct EvCache {
   uint16_t *rnd;
-  uint32_t *mask;
+  unsigned long long *mask;
   int32_t *tgt;
 };
+// mask bits 0..26: bricks (dz+1)*9 + (dy+1)*3 + (dx+1) around the saddle's
+// brick; bits 32..58: superbricks likewise for vertices farther away; bit 63:
+// a vertex outside both neighbourhoods (never reused).
+constexpr unsigned long long kFar = 1ull << 63;
 
 __device__ __forceinline__ void brick_bit(int x, int y, int z, int bsx, int bsy, int bsz,
-                                          uint32_t &mask) {
-  const int dx = (x / BX) - bsx, dy = (y / BY) - bsy, dz = (z / BZ) - bsz;
-  if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) mask |= 0x80000000u;
-  else mask |= 1u << ((dz + 1) * 9 + (dy + 1) * 3 + (dx + 1));
+                                          unsigned long long &mask) {
+  const int bx = x / BX, by = y / BY, bz = z / BZ;
+  const int dx = bx - bsx, dy = by - bsy, dz = bz - bsz;
+  if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) {
+    mask |= 1ull << ((dz + 1) * 9 + (dy + 1) * 3 + (dx + 1));
+    return;
+  }
+  const int ex = bx / SB - bsx / SB, ey = by / SB - bsy / SB, ez = bz / SB - bsz / SB;
+  if (ex >= -1 && ex <= 1 && ey >= -1 && ey <= 1 && ez >= -1 && ez <= 1)
+    mask |= 1ull << (32 + (ez + 1) * 9 + (ey + 1) * 3 + (ex + 1));
+  else
+    mask |= kFar;
 }
 
 // walk() that also records the bricks it visits (single GPU, g slots)
 template <bool UP>
 __device__ __forceinline__ int walk_track(int u, int x, int y, int z,
                                           const uint8_t *__restrict__ slots, const GridP &G,
-                                          int bsx, int bsy, int bsz, uint32_t &mask) {
+                                          int bsx, int bsy, int bsz, unsigned long long &mask) {
   const int A = G.nx * G.ny;
   int w = u;
   for (;;) {
@@ -715,7 +736,7 @@ __device__ __forceinline__ unsigned events_group(
   const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
   int best = -1;
   float bv = 0.0f;
-  uint32_t mask = 0;
+  unsigned long long mask = 0;
   if (active && l16 < kSlots) {
     const uint32_t valid = valid_mask(sx, sy, sz, G);
     if (CACHE) brick_bit(sx, sy, sz, bsx, bsy, bsz, mask);
@@ -927,17 +948,23 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
   unsigned hit = 0;
   if (k < n) {
     const uint16_t rnd = EC.rnd[k];
-    const uint32_t mask = EC.mask[k];
-    valid = rnd != 0 && !(mask >> 31);
+    const unsigned long long mask = EC.mask[k];
+    valid = rnd != 0 && !(mask & kFar);
     if (valid) {
       const int s = sl[k];
       const int sx = s % G.nx, yz = s / G.nx, sy = yz % G.ny, sz = yz / G.ny;
       const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
-      for (uint32_t m = mask; m && valid; m &= m - 1) {
+      for (uint32_t m = (uint32_t)mask; m && valid; m &= m - 1) {
         const int j = __ffs(m) - 1;
         const int dz = j / 9 - 1, dy = (j / 3) % 3 - 1, dx = j % 3 - 1;
         const int nb = (bsx + dx) + T.nbx * ((bsy + dy) + T.nby * (bsz + dz));
         if (T.bval[nb] > rnd || T.bslot[nb] > rnd) valid = false;
+      }
+      for (uint32_t m = (uint32_t)(mask >> 32); m && valid; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const int dz = j / 9 - 1, dy = (j / 3) % 3 - 1, dx = j % 3 - 1;
+        const int nb = (bsx / SB + dx) + T.nsx * ((bsy / SB + dy) + T.nsy * (bsz / SB + dz));
+        if (T.sbval[nb] > rnd || T.sbslot[nb] > rnd) valid = false;
       }
     }
     if (valid) {
@@ -1097,7 +1124,7 @@ __global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
         if (E) {
           const int wx = (int)(w - row * G.W), y = (int)(row % G.ny), z = (int)(row / G.ny);
           if (T.bval && lane == 0)
-            T.bval[wx + T.nbx * ((y / BY) + T.nby * (z / BZ))] = (uint16_t)(T.round + 1);
+            stamp(T.bval, T.sbval, T, wx, y / BY, z / BZ, (uint16_t)(T.round + 1));
           if (T.act_next && lane < 7) {
             // closed stars of the edited vertices: 7 (dz, dy) rows, x-1 / x+1
             // spill into the neighbouring words
