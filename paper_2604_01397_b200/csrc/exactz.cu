@@ -151,6 +151,31 @@ struct Ctx {
   explicit Ctx(cudaStream_t st) : s(st), arena(st) {}
   ~Ctx() {
     if (hcnt) cudaFreeHost(hcnt);
+    for (int k = 0; k < 2; ++k)
+      if (side[k]) cudaStreamDestroy(side[k]);
+    for (int k = 0; k < 3; ++k)
+      if (fj[k]) cudaEventDestroy(fj[k]);
+  }
+  // fork/join of two side streams (independent kernels of one pass)
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t fj[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t main_s = nullptr;
+  void fork() {
+    if (!side[0]) {
+      for (int k = 0; k < 2; ++k) CK(cudaStreamCreateWithFlags(&side[k], cudaStreamNonBlocking));
+      for (int k = 0; k < 3; ++k) CK(cudaEventCreateWithFlags(&fj[k], cudaEventDisableTiming));
+    }
+    main_s = s;
+    CK(cudaEventRecord(fj[0], s));
+    for (int k = 0; k < 2; ++k) CK(cudaStreamWaitEvent(side[k], fj[0], 0));
+  }
+  void on_side(int k) { s = side[k]; }
+  void join() {
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventRecord(fj[1 + k], side[k]));
+      CK(cudaStreamWaitEvent(main_s, fj[1 + k], 0));
+    }
+    s = main_s;
   }
   void init(const int64_t dims[3]) {
     keep_pool();
@@ -381,7 +406,7 @@ struct Tracking {
   int nbx = 0, nby = 0, nbz = 0, nb = 0, nsx = 0, nsy = 0, nsz = 0, nsb = 0;
   uint16_t *bval = nullptr, *bslot = nullptr, *sbval = nullptr, *sbslot = nullptr;
   EvCache ecJ{}, ecP{};
-  int *todo = nullptr, *ntodo = nullptr;
+  int *todo = nullptr, *ntodo = nullptr, *todoP = nullptr;
   void geometry(const Ctx &C) {
     nbx = (C.G.nx + BX - 1) / BX;
     nby = (C.G.ny + BY - 1) / BY;
@@ -416,8 +441,9 @@ struct Tracking {
     };
     ecJ = cache(R.nJ);
     ecP = cache(R.nP);
-    todo = C.arena.get<int>(R.nJ > R.nP ? R.nJ : R.nP);
-    ntodo = C.arena.get<int>(1);
+    todo = C.arena.get<int>(R.nJ > 0 ? R.nJ : 1);
+    ntodo = C.arena.get<int>(2);
+    todoP = C.arena.get<int>(R.nP > 0 ? R.nP : 1);
     cache_on = true;
   }
   Track track(int round) const {
@@ -468,6 +494,11 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
                                                  C.G, T, C.cnt);
     });
   }
+  // R4 and the two C3 event kernels are independent (all read the snapshot g
+  // and the slots, all only OR marks and add counters): run them on two side
+  // streams, joined before the count/edit.
+  C.fork();
+  C.on_side(1);
   if (!(flags & EXACTZ_NO_C2) && R.nS > 1) {
     C.run(EXACTZ_K_SADDLE_ORDER, 8ull * R.nS, true, [&] {
       k_saddle_order<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(g, R.S, R.nS, marks, C.G,
@@ -482,13 +513,15 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
     });
   } else if (c3 && !(flags & EXACTZ_REFORMULATED)) {
     const bool cache = trk && trk->cache_on;
+    launch_events<true, false>(C, g, R.P, R.nP, slots, R.ref, R.M1, marks,
+                               cache ? trk->ecP : EvCache{}, T, cache ? trk->todoP : nullptr,
+                               cache ? trk->ntodo + 1 : nullptr);
+    C.on_side(0);
     launch_events<false, false>(C, g, R.J, R.nJ, slots, R.ref, R.m1, marks,
                                 cache ? trk->ecJ : EvCache{}, T, cache ? trk->todo : nullptr,
                                 cache ? trk->ntodo : nullptr);
-    launch_events<true, false>(C, g, R.P, R.nP, slots, R.ref, R.M1, marks,
-                               cache ? trk->ecP : EvCache{}, T, cache ? trk->todo : nullptr,
-                               cache ? trk->ntodo : nullptr);
   }
+  C.join();
   // bytes: mark words read (the per-edit 14 B are added once V_t is known)
   C.run(EXACTZ_K_EDIT, (uint64_t)C.V / 8, true, [&] {
     if (trk)
