@@ -184,6 +184,7 @@ struct Ctx {
     G.nz = (int)dims[2];
     G.V = (int)V;
     G.W = (G.nx + 31) / 32;
+    grid_fastdiv(G);
     for (int s = 0; s < kSlots; ++s)
       G.delta[s] = kOff[s][0] + G.nx * (kOff[s][1] + G.ny * kOff[s][2]);
     G.zoff = 0;
@@ -303,18 +304,18 @@ static void sort_ids(Ctx &C, uint64_t *keys, int n, int32_t *ids) {
 
 template <bool SPLIT, bool FROM_REF>
 static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, const uint8_t *slots,
-                          const uint32_t *ref, int32_t *ext, uint32_t *marks,
+                          const uint32_t *lm, const uint32_t *ref, int32_t *ext, uint32_t *marks,
                           EvCache ec = EvCache{}, Track tr = Track{}, int *todo = nullptr,
                           int *ntodo = nullptr) {
   if (n <= 0) return;
-  const int64_t threads = (int64_t)n * 8;  // 8 lanes per saddle
+  const int64_t threads = n;  // one lane per saddle
   // algorithmic bytes: per saddle its id, its value, 14 link values, the
   // reached extrema's values and ids
   const int cls = FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS;
   if (!ec.rnd) {
     C.run(cls, 128ull * n, true, [&] {
       k_events<SPLIT, FROM_REF, false><<<(unsigned)((threads + 255) / 256), 256, 0, C.s>>>(
-          h, sl, n, slots, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt);
+          h, sl, n, slots, lm, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt);
     });
     return;
   }
@@ -324,7 +325,8 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
                                                                         C.G, todo, ntodo, C.cnt);
   });
   C.run(cls, 0, true, [&] {
-    k_events_cached<SPLIT><<<148 * 16, 256, 0, C.s>>>(h, sl, todo, ntodo, slots, ext, marks, C.G,
+    k_events_cached<SPLIT><<<148 * 16, 256, 0, C.s>>>(h, sl, todo, ntodo, slots, lm, ext, marks,
+                                                      C.G,
                                                       ec, tr, C.cnt);
   });
 }
@@ -384,8 +386,8 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
   R.M1 = C.arena.get<int32_t>(R.nP);
   // m1 / M1 by walking f's steepest paths from each saddle's link
   if (!reform) {
-    launch_events<false, true>(C, f, R.J, R.nJ, nullptr, R.ref, R.m1, nullptr);
-    launch_events<true, true>(C, f, R.P, R.nP, nullptr, R.ref, R.M1, nullptr);
+    launch_events<false, true>(C, f, R.J, R.nJ, nullptr, nullptr, R.ref, R.m1, nullptr);
+    launch_events<true, true>(C, f, R.P, R.nP, nullptr, nullptr, R.ref, R.M1, nullptr);
   }
 }
 
@@ -399,6 +401,7 @@ struct PassOut {
 struct Tracking {
   // vertex activity: act[cur] = this pass's active set (valid when `ready`)
   bool act_on = false, ready = false;
+  bool sparse = false;  // few active vertices: the sparse stencil, else the compacted one
   uint32_t *act[2] = {nullptr, nullptr};
   int cur = 0;
   // C3 cache with brick stamps
@@ -471,26 +474,35 @@ struct Tracking {
 // cached C3 results are reused while their bricks are unchanged (exact; see
 // kernels.cuh Track).
 static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float *g, uint8_t *c,
-                               uint32_t *marks, uint8_t *slots, float xi, float delta, int N,
+                               uint32_t *marks, uint8_t *slots, uint32_t *lm, float xi,
+                               float delta, int N,
                                uint32_t flags, bool do_edit, Tracking *trk = nullptr,
                                int round = 0) {
   bool c3 = !(flags & EXACTZ_NO_C3);
   C.zero();
   const Track T = trk ? trk->track(round) : Track{};
-  const bool sparse = trk && trk->ready;
+  const bool sparse = trk && trk->ready && trk->sparse;
+  const bool compact = trk && trk->ready && !trk->sparse;
   // algorithmic bytes per vertex: g 4 + ref 4 read, slots 1 + mark bits 1/8
-  // written; a sparse pass: the active vertices only
-  if (!sparse) {
+  // written; a sparse or compacted pass: the active vertices
+  // only (plus the activity bitmap)
+  if (compact) {
+    C.run(EXACTZ_K_SPARSE, (uint64_t)C.V / 8, true, [&] {
+      k_stencil_compact<<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, trk->act[trk->cur],
+                                                        C.G, C.zc, T, C.cnt);
+    });
+  } else if (!sparse) {
     C.run(EXACTZ_K_STENCIL, (uint64_t)C.V * 73 / 8, true, [&] {
       if (trk)
-        k_stencil<true><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, C.G, C.zc, T, C.cnt);
+        k_stencil<true><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G, C.zc, T,
+                                                       C.cnt);
       else
-        k_stencil<false><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, C.G, C.zc, T,
+        k_stencil<false><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G, C.zc, T,
                                                         C.cnt);
     });
   } else {
     C.run(EXACTZ_K_SPARSE, (uint64_t)C.V / 8, true, [&] {
-      k_stencil_sparse<<<148 * 8, 256, 0, C.s>>>(g, R.ref, marks, slots, trk->act[trk->cur],
+      k_stencil_sparse<<<148 * 8, 256, 0, C.s>>>(g, R.ref, marks, slots, lm, trk->act[trk->cur],
                                                  C.G, T, C.cnt);
     });
   }
@@ -513,11 +525,11 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
     });
   } else if (c3 && !(flags & EXACTZ_REFORMULATED)) {
     const bool cache = trk && trk->cache_on;
-    launch_events<true, false>(C, g, R.P, R.nP, slots, R.ref, R.M1, marks,
+    launch_events<true, false>(C, g, R.P, R.nP, slots, lm, R.ref, R.M1, marks,
                                cache ? trk->ecP : EvCache{}, T, cache ? trk->todoP : nullptr,
                                cache ? trk->ntodo + 1 : nullptr);
     C.on_side(0);
-    launch_events<false, false>(C, g, R.J, R.nJ, slots, R.ref, R.m1, marks,
+    launch_events<false, false>(C, g, R.J, R.nJ, slots, lm, R.ref, R.m1, marks,
                                 cache ? trk->ecJ : EvCache{}, T, cache ? trk->todo : nullptr,
                                 cache ? trk->ntodo : nullptr);
   }
@@ -589,6 +601,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   uint8_t *c = (opts && opts->edit_counts) ? opts->edit_counts : C.arena.get<uint8_t>(V);
   uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
   uint8_t *slots = C.arena.get<uint8_t>(V);
+  uint32_t *lm = C.arena.get<uint32_t>(V);
   CK(cudaMemsetAsync(c, 0, V, s));
   CK(cudaMemsetAsync(marks, 0, C.mark_words() * sizeof(uint32_t), s));
   CK(cudaEventRecord(e1, s));
@@ -606,22 +619,32 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     const char *e = std::getenv("EXACTZ_CACHE_DIV");  // tuning knob (default 4)
     return e ? std::strtoull(e, nullptr, 10) : 4ull;
   }();
+  static const unsigned long long compact_div = [] {
+    const char *e = std::getenv("EXACTZ_COMPACT_DIV");  // tuning knob (default 32)
+    return e ? std::strtoull(e, nullptr, 10) : 32ull;
+  }();
   unsigned long long prev_vt = (unsigned long long)V;
   const bool allow_track = !(flags & EXACTZ_NO_TRACK);
   for (;;) {
     bool may_edit = !(max_iters && it >= max_iters);
     const int round = (int)rows + 1;  // stamps are 16-bit pass numbers
     if (allow_track && rows >= 1 && round < 65000) {
-      // vertex activity once < 1/64 of the vertices are marked; the C3 cache
-      // once the marks are sparse at brick scale
-      if (!(flags & 0x100u) && !trk.act_on && prev_vt * act_div <= (unsigned long long)V)
+      // vertex activity once < V/compact_div vertices are marked (compacted
+      // dense passes; the sparse stencil below V/act_div); the C3 cache once
+      // the marks are sparse at brick scale
+      // (debug flag 0x400: compacted passes from the second pass on, never
+      // the sparse stencil)
+      const bool force_compact = (flags & 0x400u) != 0;
+      trk.sparse = !force_compact && prev_vt * act_div <= (unsigned long long)V;
+      if (!(flags & 0x100u) && !trk.act_on &&
+          (force_compact || trk.sparse || prev_vt * compact_div <= (unsigned long long)V))
         trk.start_act(C);
       if (!(flags & (0x200u | EXACTZ_REFORMULATED)) && !trk.cache_on &&
           prev_vt * cache_div <= (unsigned long long)trk.nb)
         trk.start_cache(C, R);
     }
     const bool tracked = allow_track && round < 65000 && (trk.act_on || trk.cache_on);
-    PassOut o = detect_and_edit(C, R, f, out, c, marks, slots, eps, delta, N, flags, may_edit,
+    PassOut o = detect_and_edit(C, R, f, out, c, marks, slots, lm, eps, delta, N, flags, may_edit,
                                 tracked ? &trk : nullptr, round);
     prev_vt = o.vt;
     if (stats && stats->rows && rows < stats->cap) {
@@ -747,8 +770,9 @@ exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3]
     build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
     uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
     uint8_t *slots = C.arena.get<uint8_t>(V);
+  uint32_t *lm = C.arena.get<uint32_t>(V);
     CK(cudaMemsetAsync(marks, 0, C.mark_words() * sizeof(uint32_t), s));
-    PassOut o = detect_and_edit(C, R, f, const_cast<float *>(g), nullptr, marks, slots, eps_abs,
+    PassOut o = detect_and_edit(C, R, f, const_cast<float *>(g), nullptr, marks, slots, lm, eps_abs,
                                 0.0f, 5, flags, false);
     *violations = o.vt;
     if (row) {

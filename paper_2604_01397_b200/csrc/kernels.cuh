@@ -56,7 +56,27 @@ struct GridP {
   int delta[kSlots];  // linear offset of each slot
   int zoff, gnz;      // global z of local plane 0, global nz
   int zb, ze;         // owned local planes [zb, ze)
+  uint32_t mnx, mny;  // division by nx, ny: q = (umulhi(n, m) + n) >> l (n < 2^31)
+  int lnx, lny;
 };
+
+// Magic numbers of the unsigned division n / d for n < 2^31, d >= 1
+// (Granlund-Montgomery): l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1.
+inline void fastdiv_magic(uint32_t d, uint32_t &m, int &l) {
+  l = 0;
+  while ((1ull << l) < d) ++l;
+  m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
+}
+inline void grid_fastdiv(GridP &G) {
+  fastdiv_magic((uint32_t)G.nx, G.mnx, G.lnx);
+  fastdiv_magic((uint32_t)G.ny, G.mny, G.lny);
+}
+__device__ __forceinline__ int div_nx(int n, const GridP &G) {
+  return (int)((__umulhi((uint32_t)n, G.mnx) + (uint32_t)n) >> G.lnx);
+}
+__device__ __forceinline__ int div_ny(int n, const GridP &G) {
+  return (int)((__umulhi((uint32_t)n, G.mny) + (uint32_t)n) >> G.lny);
+}
 
 // Change tracking (single GPU, late rounds).
 //  * Vertex activity: a vertex whose closed star saw no value change and that
@@ -102,6 +122,22 @@ __host__ __device__ constexpr bool ref_join(uint32_t r) { return (r >> 29) & 1; 
 __host__ __device__ constexpr bool ref_split(uint32_t r) { return (r >> 30) & 1; }
 
 // slots of vertex (x, y, local z) whose neighbour exists in the global domain
+// (split into the x/y and the z conditions for the z-marching kernels)
+__device__ __forceinline__ uint32_t valid_xy(int x, int y, const GridP &G) {
+  uint32_t m = 0x3FFFu;
+  if (x == 0) m &= ~(uint32_t)c_link.req[0];
+  if (x == G.nx - 1) m &= ~(uint32_t)c_link.req[1];
+  if (y == 0) m &= ~(uint32_t)c_link.req[2];
+  if (y == G.ny - 1) m &= ~(uint32_t)c_link.req[3];
+  return m;
+}
+__device__ __forceinline__ uint32_t valid_z(int z, const GridP &G) {
+  uint32_t m = 0x3FFFu;
+  const int zg = z + G.zoff;
+  if (zg == 0) m &= ~(uint32_t)c_link.req[4];
+  if (zg == G.gnz - 1) m &= ~(uint32_t)c_link.req[5];
+  return m;
+}
 __device__ __forceinline__ uint32_t valid_mask(int x, int y, int z, const GridP &G) {
   uint32_t m = 0x3FFFu;
   const int zg = z + G.zoff;
@@ -192,8 +228,15 @@ __device__ __forceinline__ Star eval_star(const float *__restrict__ h, int i, ui
   return eval_values(v, h[i]);
 }
 
+// linear offset of slot s (0..13) by arithmetic decode (no indexed parameter
+// loads for a data-dependent slot)
+__device__ __forceinline__ int slot_delta(int s, const GridP &G) {
+  const int b = slot_bits(s);
+  const int d = (b & 1) + ((b >> 1) & 1) * G.nx + (b >> 2) * (G.nx * G.ny);
+  return s >= 7 ? d : -d;
+}
 __device__ __forceinline__ int slot_target(int i, int slot, const GridP &G) {
-  return slot == kSelf ? i : i + G.delta[slot];
+  return slot == kSelf ? i : i + slot_delta(slot, G);
 }
 
 __device__ __forceinline__ void warp_add(unsigned long long *dst, unsigned v) {
@@ -210,7 +253,7 @@ __device__ __forceinline__ uint32_t ordered_key(float v) {
 
 // mark bitmap: row-padded, bit x of word row*W + x/32 (row = y + ny*z)
 __device__ __forceinline__ void mark_vertex(uint32_t *marks, int v, const GridP &G) {
-  int x = v % G.nx, row = v / G.nx;
+  const int row = div_nx(v, G), x = v - row * G.nx;
   atomicOr(&marks[(size_t)row * G.W + (x >> 5)], 1u << (x & 31));
 }
 
@@ -345,24 +388,78 @@ __device__ __forceinline__ void store_plane_regs(float *sg, const float (&r)[2])
   }
 }
 
-// Shared marks of one plane buffer: for every row ly (0..SY-1) the 7 row masks
-// (dz, dy) a warp can produce; word [ly][k] is written by exactly one warp
-// (row ly-1-dy_k) in exactly one step (plane P-dz_k), so plain stores suffice.
-typedef unsigned long long u64;
-constexpr int KR = 7;  // (dz,dy) = (-1,-1) (-1,0) (0,-1) (0,0) (0,1) (1,0) (1,1)
+// R1, R2, R3 at one vertex (x, y, z) from its closed star in the shared ring
+// (pm, p0, pp: the vertex's cell in planes z-1, z, z+1) and its ref word r.
+// Returns the targets as a 15-bit mask over the closed star (bit 14 = self);
+// ns receives the packed steepest slots (dn | up << 4), lower the g-lower
+// mask.  At the f-saddles the stencils keep lm = lower | upper << 16 (the
+// g-lower and g-upper link slots) for the C3 event kernels.
+__device__ __forceinline__ uint32_t stencil_rules(const float *pm, const float *p0,
+                                                  const float *pp, uint32_t r, uint32_t valid,
+                                                  unsigned &n1,
+                                                  unsigned &n2, unsigned &n3, uint8_t &ns,
+                                                  uint32_t &lower) {
+  float v[kSlots];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {  // s is a compile-time constant here
+    const int b = slot_bits(s), sg1 = slot_sign(s);
+    const float *pl = (b >> 2) ? (sg1 > 0 ? pp : pm) : p0;
+    v[s] = pl[sg1 * ((b & 1) + ((b >> 1) & 1) * SX)];
+  }
+  const Star st = eval_values(v, *p0);
+  uint32_t tgt = 0;
+  // R1: the g-largest neighbour is an impostor -> decrease it
+  if (st.up != ref_up(r)) { tgt |= 1u << st.up; n1 += 1; }
+  // R2: the g-smallest neighbour changed -> decrease the true N_min
+  if (st.dn != ref_dn(r)) { tgt |= 1u << ref_dn(r); n2 += 1; }
+  // R3 (amb-7, amb-8): flipped pairs at f-saddles and at
+  // vertices whose type (nlc, nuc) changed; target = the f-smaller end
+  const uint32_t flow = ref_flow(r);
+  const uint32_t flip = st.lower ^ flow;
+  if (flip) {
+    bool apply = ref_saddle(r);
+    if (!apply) {
+      int nl, nu;
+      link_type(st.lower, valid, nl, nu);
+      apply = (nl != ref_nlc(r)) || (nu != ref_nuc(r));
+    }
+    if (apply) {
+      n3 += __popc(flip);
+      tgt |= flip & flow;
+      if (flip & ~flow) tgt |= 1u << kSelf;
+    }
+  }
+  ns = (uint8_t)(st.dn | (st.up << 4));
+  lower = st.lower;
+  return tgt;
+}
 
-// Flush (and clear) plane buffer `rows` of plane p into the global bitmap.
-// One warp: lane ly < SY ORs the 7 words of row ly and issues at most 3
-// atomics (left halo bit, 32 interior bits, right halo bit).
-__device__ __forceinline__ void flush_plane(uint32_t *__restrict__ marks, u64 (*rows)[KR], int p,
+// Row masks of the marks, by writer: step z (mod 4) x warp (y row) x the 7
+// (dz, dy) target rows, one u64 each (bit 1 + dx + lane; 8th word padding).
+// Lane 0 of every warp stores its 7 words every step (zeros when it marked
+// nothing); the flush of plane p ORs the words its writers stored at steps
+// p+1, p, p-1.
+typedef unsigned long long u64;
+constexpr int KR = 7;  // k: (dz,dy) = (-1,-1) (-1,0) (0,-1) (0,0) (0,1) (1,0) (1,1)
+__host__ __device__ constexpr int kr_dz(int k) { return k < 2 ? -1 : (k < 5 ? 0 : 1); }
+__host__ __device__ constexpr int kr_dy(int k) {
+  return (k == 0 || k == 2) ? -1 : ((k == 4 || k == 6) ? 1 : 0);
+}
+
+// Flush plane p (rows ly = 0..SY-1 of the tile with its halo) into the global
+// bitmap: lane ly ORs the words of its writers and issues at most 3 atomics
+// (left halo bit, the 32 interior bits, right halo bit).  Writer steps
+// outside [z0, z1) did not run and are skipped.
+__device__ __forceinline__ void flush_plane(uint32_t *__restrict__ marks,
+                                            const u64 (*wr)[TY][8], int p, int z0, int z1,
                                             int x0, int y0, const GridP &G) {
   const int ly = threadIdx.x;
   if (ly >= SY) return;
   u64 val = 0;
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
-    val |= rows[ly][k];
-    rows[ly][k] = 0ull;
+    const int w = ly - 1 - kr_dy(k), st = p - kr_dz(k);
+    if (w >= 0 && w < TY && st >= z0 && st < z1) val |= wr[st & 3][w][k];
   }
   const int gy = y0 - 1 + ly;
   if (!val || gy < 0 || gy >= G.ny || p < 0 || p >= G.nz) return;
@@ -374,33 +471,34 @@ __device__ __forceinline__ void flush_plane(uint32_t *__restrict__ marks, u64 (*
   if (((val >> 33) & 1ull) && x0 + 32 < G.nx) atomicOr(&row[wx + 1], 1u);
 }
 
-// R1, R2, R3 at every vertex from its closed star in g and its ref word;
-// writes the packed steepest slots (dn | up << 4) used by the label walks.
+// Dense pass: R1, R2, R3 at every vertex; writes the packed steepest slots
+// used by the label walks.
 template <bool TRACK>
 __global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
                                                    const uint32_t *__restrict__ ref,
                                                    uint32_t *__restrict__ marks,
-                                                   uint8_t *__restrict__ slots, GridP G, int zc,
+                                                   uint8_t *__restrict__ slots,
+                                                   uint32_t *__restrict__ lm, GridP G, int zc,
                                                    Track T, unsigned long long *cnt) {
   __shared__ float sg[4][SP];
-  __shared__ u64 smk[4][SY][KR];
+  __shared__ __align__(16) u64 wr[4][TY][8];
   const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const int tx = threadIdx.x, ty = threadIdx.y;
   const int x0 = bx * TX, y0 = by * TY;
   const int z0 = G.zb + bz * zc, z1 = min(z0 + zc, G.ze);
   const int x = x0 + tx, y = y0 + ty;
   const bool inside = x < G.nx && y < G.ny;
   const int c = (ty + 1) * SX + tx + 1;
+  const uint32_t vxy = valid_xy(x, y, G);
   unsigned n1 = 0, n2 = 0, n3 = 0;
   const PlaneCells pc = plane_cells(x0, y0, G);
 
-  {  // prologue: planes z0-1, z0, z0+1 (NaN outside the domain), cleared marks
+  {  // prologue: planes z0-1, z0, z0+1 (NaN outside the domain)
     float r[2];
     for (int p = z0 - 1; p <= z0 + 1; ++p) {
       load_plane_regs(g, p, pc, G, r);
       store_plane_regs(sg[p & 3], r);
     }
-    for (int k = tid; k < 4 * SY * KR; k += NT) (&smk[0][0][0])[k] = 0ull;
   }
   __syncthreads();
 
@@ -410,91 +508,219 @@ __global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
     const bool prefetch = pz <= z1;
     if (prefetch) load_plane_regs(g, pz, pc, G, pre);
 
-    uint32_t tgt = 0;  // targets as a 15-bit mask over the closed star (bit 14 = self)
+    uint32_t tgt = 0;
     bool schg = false;
     if (inside) {
       const int i = x + G.nx * (y + G.ny * z);
-      const float *pm = &sg[(z - 1) & 3][c], *p0 = &sg[z & 3][c], *pp = &sg[(z + 1) & 3][c];
-      float v[kSlots];
-#pragma unroll
-      for (int s = 0; s < kSlots; ++s) {  // s is a compile-time constant here
-        const int b = slot_bits(s), sg1 = slot_sign(s);
-        const float *pl = (b >> 2) ? (sg1 > 0 ? pp : pm) : p0;
-        v[s] = pl[sg1 * ((b & 1) + ((b >> 1) & 1) * SX)];
-      }
-      const float hc = *p0;
-      const Star st = eval_values(v, hc);
       const uint32_t r = __ldcs(&ref[i]);
-      // R1: the g-largest neighbour is an impostor -> decrease it
-      if (st.up != ref_up(r)) { tgt |= 1u << st.up; n1 += 1; }
-      // R2: the g-smallest neighbour changed -> decrease the true N_min
-      if (st.dn != ref_dn(r)) { tgt |= 1u << ref_dn(r); n2 += 1; }
-      // R3 (amb-7, amb-8): flipped pairs at f-saddles and at
-      // vertices whose type (nlc, nuc) changed; target = the f-smaller end
-      const uint32_t flow = ref_flow(r);
-      const uint32_t flip = st.lower ^ flow;
-      if (flip) {
-        bool apply = ref_saddle(r);
-        if (!apply) {
-          int nl, nu;
-          link_type(st.lower, valid_mask(x, y, z, G), nl, nu);
-          apply = (nl != ref_nlc(r)) || (nu != ref_nuc(r));
-        }
-        if (apply) {
-          n3 += __popc(flip);
-          tgt |= flip & flow;
-          if (flip & ~flow) tgt |= 1u << kSelf;
-        }
-      }
-      const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
+      uint8_t ns;
+      uint32_t lower;
+      const uint32_t valid = vxy & valid_z(z, G);
+      tgt = stencil_rules(&sg[(z - 1) & 3][c], &sg[z & 3][c], &sg[(z + 1) & 3][c], r, valid, n1,
+                          n2, n3, ns, lower);
       if (TRACK && T.bval) schg = (slots[i] != ns);
       slots[i] = ns;
+      if (ref_saddle(r)) lm[i] = lower | ((valid & ~lower) << 16);
     }
     if (TRACK && T.bval) {  // slot-change stamp of this warp's brick
       const unsigned chg = __ballot_sync(0xffffffffu, schg);
       if (tx == 0 && chg) stamp(T.bslot, T.sbslot, T, bx, y / BY, z / BZ, (uint16_t)T.round);
-      schg = false;
     }
     if (TRACK && T.act_next) {  // fired vertices stay active next pass
       const unsigned fired = __ballot_sync(0xffffffffu, tgt != 0);
       if (tx == 0 && fired) atomicOr(&T.act_next[(size_t)(y + G.ny * z) * G.W + bx], fired);
     }
-    // warp-aggregated marks: one ballot per slot, shifted into 7 row masks
+    // warp-aggregated marks: one ballot per slot, shifted into the 7 row masks
+    u64 rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (__any_sync(0xffffffffu, tgt)) {
       uint32_t bal[15];
 #pragma unroll
-      for (int s = 0; s < 15; ++s) bal[s] = __ballot_sync(0xffffffffu, (tgt >> s) & 1u);
+      for (int s = 0; s < 15; ++s) bal[s] = __ballot_sync(0xffffffffu, tgt & (1u << s));
       // bit position = 1 + dx (lane 0 <-> lx 1)
-      const u64 rv[KR] = {
-          (u64)bal[0] | ((u64)bal[1] << 1),                        // (-1,-1): slots 0, 1
-          (u64)bal[2] | ((u64)bal[3] << 1),                        // (-1, 0): slots 2, 3
-          (u64)bal[4] | ((u64)bal[5] << 1),                        // ( 0,-1): slots 4, 5
-          (u64)bal[6] | ((u64)bal[14] << 1) | ((u64)bal[7] << 2),  // ( 0, 0): 6, self, 7
-          ((u64)bal[8] << 1) | ((u64)bal[9] << 2),                 // ( 0, 1): slots 8, 9
-          ((u64)bal[10] << 1) | ((u64)bal[11] << 2),               // ( 1, 0): slots 10, 11
-          ((u64)bal[12] << 1) | ((u64)bal[13] << 2)};              // ( 1, 1): slots 12, 13
-      if (tx < KR) {
-        const int dz = tx < 2 ? -1 : (tx < 5 ? 0 : 1);
-        const int dy = (tx == 0 || tx == 2) ? -1 : ((tx == 4 || tx == 6) ? 1 : 0);
-        u64 val = 0;
-#pragma unroll
-        for (int k = 0; k < KR; ++k) val = (k == tx) ? rv[k] : val;
-        smk[(z + dz) & 3][ty + 1 + dy][tx] = val;
-      }
+      rv[0] = (u64)bal[0] | ((u64)bal[1] << 1);                        // (-1,-1): slots 0, 1
+      rv[1] = (u64)bal[2] | ((u64)bal[3] << 1);                        // (-1, 0): slots 2, 3
+      rv[2] = (u64)bal[4] | ((u64)bal[5] << 1);                        // ( 0,-1): slots 4, 5
+      rv[3] = (u64)bal[6] | ((u64)bal[14] << 1) | ((u64)bal[7] << 2);  // ( 0, 0): 6, self, 7
+      rv[4] = ((u64)bal[8] << 1) | ((u64)bal[9] << 2);                 // ( 0, 1): slots 8, 9
+      rv[5] = ((u64)bal[10] << 1) | ((u64)bal[11] << 2);               // ( 1, 0): slots 10, 11
+      rv[6] = ((u64)bal[12] << 1) | ((u64)bal[13] << 2);               // ( 1, 1): slots 12, 13
     }
-    // plane z-2 is complete (its contributors z-3 .. z-1 are done): one warp
+    if (tx == 0) {
+      ulonglong2 *d = reinterpret_cast<ulonglong2 *>(&wr[z & 3][ty][0]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d[k] = make_ulonglong2(rv[2 * k], rv[2 * k + 1]);
+    }
+    // plane z-2 is complete (its writers z-3 .. z-1 are done): one warp
     // flushes it
     const int pf = z - 2;
-    if (ty == (z & (TY - 1)) && pf >= z0 - 1 && pf >= 0)
-      flush_plane(marks, smk[pf & 3], pf, x0, y0, G);
+    if (ty == (z & (TY - 1)) && pf >= z0 - 1 && pf >= 0) flush_plane(marks, wr, pf, z0, z1, x0, y0, G);
     if (prefetch) store_plane_regs(sg[pz & 3], pre);
     __syncthreads();
   }
   // epilogue: planes z1-2 .. z1 not flushed by the loop (one warp each)
   {
     const int pf = z1 - 2 + ty;
-    if (ty < 3 && pf >= z0 - 1 && pf >= 0 && pf < G.nz)
-      flush_plane(marks, smk[pf & 3], pf, x0, y0, G);
+    if (ty < 3 && pf >= z0 - 1 && pf >= 0 && pf < G.nz) flush_plane(marks, wr, pf, z0, z1, x0, y0, G);
+  }
+
+  warp_add(&cnt[C_N1 + 0], n1);
+  warp_add(&cnt[C_N1 + 1], n2);
+  warp_add(&cnt[C_N1 + 2], n3);
+}
+
+// Compacted dense pass (tracking, moderately many active vertices): the same
+// z-march and shared ring, but per plane only the active vertices of the tile
+// are evaluated, packed onto the first threads of the CTA.  The list of plane
+// z+1 is built during step z from the activity words (consumed words are
+// cleared); marks go to per-plane shared row words by shared atomics; the
+// fired vertices of plane z are written to act_next at step z+1; a brick's
+// slot-change stamp comes from the step's barrier (__syncthreads_or).
+__global__ void __launch_bounds__(NT, 5) k_stencil_compact(const float *__restrict__ g,
+                                                           const uint32_t *__restrict__ ref,
+                                                           uint32_t *__restrict__ marks,
+                                                           uint8_t *__restrict__ slots,
+                                                           uint32_t *__restrict__ lm,
+                                                           uint32_t *__restrict__ act, GridP G,
+                                                           int zc, Track T,
+                                                           unsigned long long *cnt) {
+  __shared__ float sg[4][SP];
+  __shared__ uint32_t cmI[4][SY], cmH[4][SY];  // interior bits / halo bits (1: x0-1, 2: x0+32)
+  __shared__ uint16_t list[4][NT];
+  __shared__ int ln[4];
+  __shared__ uint32_t fm[2][TY];
+  const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const int x0 = bx * TX, y0 = by * TY;
+  const int z0 = G.zb + bz * zc, z1 = min(z0 + zc, G.ze);
+  const int yw = y0 + ty;  // this warp's row for the list building
+  const uint32_t xin = (G.nx - x0 >= 32) ? 0xffffffffu : ((1u << (G.nx - x0)) - 1u);
+  unsigned n1 = 0, n2 = 0, n3 = 0;
+  const PlaneCells pc = plane_cells(x0, y0, G);
+
+  // active lanes of this warp's row in plane p -> list[p & 3]
+  auto build = [&](int p) {
+    uint32_t a = 0;
+    if (yw < G.ny) {
+      uint32_t *aw = &act[(size_t)(yw + G.ny * p) * G.W + bx];
+      a = *aw;  // warp-uniform address: one broadcast load
+      if (a && tx == 0) *aw = 0u;  // consumed
+      a &= xin;
+    }
+    if (!a) return;
+    int base = 0;
+    if (tx == 0) base = atomicAdd(&ln[p & 3], __popc(a));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((a >> tx) & 1u) list[p & 3][base + __popc(a & ((1u << tx) - 1u))] = (uint16_t)tid;
+  };
+
+  if (tid < 4) ln[tid] = 0;
+  if (tid < 4 * SY) {
+    (&cmI[0][0])[tid] = 0u;
+    (&cmH[0][0])[tid] = 0u;
+  }
+  if (tid < 2 * TY) (&fm[0][0])[tid] = 0u;
+  {  // prologue: planes z0-1, z0, z0+1 (NaN outside the domain)
+    float r[2];
+    for (int p = z0 - 1; p <= z0 + 1; ++p) {
+      load_plane_regs(g, p, pc, G, r);
+      store_plane_regs(sg[p & 3], r);
+    }
+  }
+  __syncthreads();
+  build(z0);
+  __syncthreads();
+
+  for (int z = z0; z < z1; ++z) {
+    float pre[2];
+    const int pz = z + 2;
+    const bool prefetch = pz <= z1;
+    if (prefetch) load_plane_regs(g, pz, pc, G, pre);
+    if (z + 1 < z1) build(z + 1);
+    if (tid == 0) ln[(z + 2) & 3] = 0;  // plane z-2's count, reused by plane z+2
+    if (z > z0 && tx == 0) {  // fired vertices of plane z-1 (complete at the last barrier)
+      uint32_t &w = fm[(z - 1) & 1][ty];
+      if (w) {
+        atomicOr(&T.act_next[(size_t)(yw + G.ny * (z - 1)) * G.W + bx], w);
+        w = 0u;
+      }
+    }
+
+    bool schg = false;
+    if (tid < ln[z & 3]) {
+      const int cell = list[z & 3][tid];
+      const int lx = cell & 31, ly = cell >> 5;
+      const int x = x0 + lx, y = y0 + ly;
+      const int i = x + G.nx * (y + G.ny * z);
+      const int c = (ly + 1) * SX + lx + 1;
+      const uint32_t r = ref[i];
+      uint8_t ns;
+      uint32_t lower;
+      const uint32_t valid = valid_mask(x, y, z, G);
+      const uint32_t tgt = stencil_rules(&sg[(z - 1) & 3][c], &sg[z & 3][c],
+                                         &sg[(z + 1) & 3][c], r, valid, n1, n2, n3, ns, lower);
+      if (T.bval) schg = (slots[i] != ns);
+      slots[i] = ns;
+      if (ref_saddle(r)) lm[i] = lower | ((valid & ~lower) << 16);
+      if (tgt) {
+        atomicOr(&fm[z & 1][ly], 1u << lx);
+        for (uint32_t m = tgt; m; m &= m - 1) {
+          const int s = __ffs(m) - 1;
+          int dx = 0, dy = 0, dz = 0;
+          if (s != kSelf) {
+            const int b = slot_bits(s), sg1 = slot_sign(s);
+            dx = sg1 * (b & 1);
+            dy = sg1 * ((b >> 1) & 1);
+            dz = sg1 * (b >> 2);
+          }
+          const int tx2 = lx + dx, row = ly + 1 + dy, pl = (z + dz) & 3;
+          if (tx2 < 0) atomicOr(&cmH[pl][row], 1u);
+          else if (tx2 > 31) atomicOr(&cmH[pl][row], 2u);
+          else atomicOr(&cmI[pl][row], 1u << tx2);
+        }
+      }
+    }
+    // plane z-2 is complete (its writers z-3 .. z-1 are done): one warp
+    // flushes and clears it
+    const int pf = z - 2;
+    if (ty == (z & (TY - 1)) && pf >= z0 - 1 && pf >= 0 && tx < SY) {
+      const int ly = tx, gy = y0 - 1 + ly;
+      const uint32_t w = cmI[pf & 3][ly], h = cmH[pf & 3][ly];
+      cmI[pf & 3][ly] = 0u;
+      cmH[pf & 3][ly] = 0u;
+      if ((w | h) && gy >= 0 && gy < G.ny && pf < G.nz) {
+        uint32_t *row = marks + (size_t)(gy + G.ny * pf) * G.W;
+        const int wx = x0 >> 5;
+        if (w) atomicOr(&row[wx], w);
+        if ((h & 1u) && x0 > 0) atomicOr(&row[wx - 1], 0x80000000u);
+        if ((h & 2u) && x0 + 32 < G.nx) atomicOr(&row[wx + 1], 1u);
+      }
+    }
+    if (prefetch) store_plane_regs(sg[pz & 3], pre);
+    if (T.bval) {
+      if (__syncthreads_or(schg) && tid == 0)
+        stamp(T.bslot, T.sbslot, T, bx, y0 / BY, z / BZ, (uint16_t)T.round);
+    } else {
+      __syncthreads();
+    }
+  }
+  // epilogue: fired words of plane z1-1; planes z1-2 .. z1 not flushed yet
+  if (tx == 0 && z1 > z0) {
+    const uint32_t w = fm[(z1 - 1) & 1][ty];
+    if (w) atomicOr(&T.act_next[(size_t)(yw + G.ny * (z1 - 1)) * G.W + bx], w);
+  }
+  {
+    const int pf = z1 - 2 + ty;
+    if (ty < 3 && pf >= z0 - 1 && pf >= 0 && pf < G.nz && tx < SY) {
+      const int ly = tx, gy = y0 - 1 + ly;
+      const uint32_t w = cmI[pf & 3][ly], h = cmH[pf & 3][ly];
+      if ((w | h) && gy >= 0 && gy < G.ny) {
+        uint32_t *row = marks + (size_t)(gy + G.ny * pf) * G.W;
+        const int wx = x0 >> 5;
+        if (w) atomicOr(&row[wx], w);
+        if ((h & 1u) && x0 > 0) atomicOr(&row[wx - 1], 0x80000000u);
+        if ((h & 2u) && x0 + 32 < G.nx) atomicOr(&row[wx + 1], 1u);
+      }
+    }
   }
 
   warp_add(&cnt[C_N1 + 0], n1);
@@ -509,6 +735,7 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
                                                         const uint32_t *__restrict__ ref,
                                                         uint32_t *__restrict__ marks,
                                                         uint8_t *__restrict__ slots,
+                                                        uint32_t *__restrict__ lm,
                                                         uint32_t *__restrict__ act, GridP G,
                                                         Track T, unsigned long long *cnt) {
   const int lane = threadIdx.x & 31;
@@ -554,6 +781,7 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
       const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
       schg = slots[i] != ns;
       slots[i] = ns;
+      if (ref_saddle(r)) lm[i] = st.lower | ((valid & ~st.lower) << 16);
     }
     if (T.bval) {
       const unsigned chg = __ballot_sync(0xffffffffu, schg);
@@ -719,19 +947,20 @@ __device__ __forceinline__ int walk_track(int u, int x, int y, int z,
 template <bool SPLIT, bool FROM_REF, bool CACHE, bool SLAB>
 __device__ __forceinline__ unsigned events_group(
     int k, bool active, const float *__restrict__ h, const int32_t *__restrict__ sl,
-    const uint8_t *__restrict__ slots, const uint32_t *__restrict__ ref, int32_t *ref_ext,
-    uint32_t *marks, const GridP &G, const Slabs &S, int32_t *remote, const EvCache &EC,
-    const Track &T, unsigned long long *cnt) {
+    const uint8_t *__restrict__ slots, const uint32_t *__restrict__ lm,
+    const uint32_t *__restrict__ ref, int32_t *ref_ext, uint32_t *marks, const GridP &G,
+    const Slabs &S, int32_t *remote, const EvCache &EC, const Track &T,
+    unsigned long long *cnt) {
   const int l16 = threadIdx.x & 15;
   const unsigned gmask = 0xffffu << (threadIdx.x & 16);  // this 16-lane group
   const int A = G.nx * G.ny, off = G.zoff * A;
   int s = 0, sx = 0, sy = 0, sz = 0;
   if (active) {
     s = __ldg(&sl[k]) - off;  // local
-    sx = s % G.nx;
-    const int yz = s / G.nx;
-    sy = yz % G.ny;
-    sz = yz / G.ny;
+    const int yz = div_nx(s, G);
+    sx = s - yz * G.nx;
+    sz = div_ny(yz, G);
+    sy = yz - sz * G.ny;
   }
   const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
   int best = -1;
@@ -741,9 +970,14 @@ __device__ __forceinline__ unsigned events_group(
     const uint32_t valid = valid_mask(sx, sy, sz, G);
     if (CACHE) brick_bit(sx, sy, sz, bsx, bsy, bsz, mask);
     if (valid & (1u << l16)) {
-      const int u = s + G.delta[l16];
-      const float hs = h[s], hu = h[u];
-      const bool lower = (l16 < 7) ? (hu <= hs) : (hu < hs);
+      const int u = s + slot_delta(l16, G);
+      bool lower;
+      if (FROM_REF) {
+        const float hs = h[s], hu = h[u];
+        lower = (l16 < 7) ? (hu <= hs) : (hu < hs);
+      } else {
+        lower = (__ldg(&lm[s]) >> l16) & 1u;  // the stencil's g-lower mask of s
+      }
       const int bb = slot_bits(l16), sg1 = slot_sign(l16);
       const int ux = sx + sg1 * (bb & 1), uy = sy + sg1 * ((bb >> 1) & 1),
                 uz = sz + sg1 * (bb >> 2);
@@ -799,9 +1033,12 @@ __device__ __forceinline__ unsigned events_group(
   return hit;
 }
 
-// Same rules with 8 lanes per saddle: lane l handles slots l and l + 8 and
-// walks both paths interleaved (two independent loads in flight per lane);
-// four saddles per warp halve the issue cost of the per-saddle work.
+// Same rules, one lane per saddle (the walks are short: a few steps on
+// average, so per-lane serial walks keep the issue cost per saddle low).  The
+// walk set comes from the stencil's link masks at s (g) or from the f values
+// (reference); two walks are in flight per lane (independent loads), each
+// taking the next slot of the set when it finishes.  Pointer steps decode a
+// nibble through a 16-entry shared table of linear offsets (kSelf -> 0).
 template <bool UP, bool FROM_REF>
 __device__ __forceinline__ int next_slot(int w, const uint8_t *__restrict__ slots,
                                          const uint32_t *__restrict__ ref) {
@@ -810,100 +1047,88 @@ __device__ __forceinline__ int next_slot(int w, const uint8_t *__restrict__ slot
 }
 
 template <bool SPLIT, bool FROM_REF, bool SLAB>
-__device__ __forceinline__ unsigned events_group8(
-    int k, bool active, const float *__restrict__ h, const int32_t *__restrict__ sl,
-    const uint8_t *__restrict__ slots, const uint32_t *__restrict__ ref, int32_t *ref_ext,
-    uint32_t *marks, const GridP &G, const Slabs &S, int32_t *remote, unsigned long long *cnt) {
-  const int l8 = threadIdx.x & 7;
-  const unsigned gmask = 0xffu << (threadIdx.x & 24);
+__global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
+                                                const int32_t *__restrict__ sl, int n,
+                                                const uint8_t *__restrict__ slots,
+                                                const uint32_t *__restrict__ lm,
+                                                const uint32_t *__restrict__ ref,
+                                                int32_t *ref_ext, uint32_t *marks, GridP G,
+                                                Slabs S, int32_t *remote,
+                                                unsigned long long *cnt) {
+  __shared__ int soff[16];
+  if (threadIdx.x < 16) soff[threadIdx.x] = threadIdx.x < kSlots ? slot_delta(threadIdx.x, G) : 0;
+  __syncthreads();
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int A = G.nx * G.ny, off = G.zoff * A, lo = G.zb * A, hi = G.ze * A;
-  int best = -1;
-  float bv = 0.0f;
-  if (active) {
+  unsigned hit = 0;
+  if (k < n) {
     const int s = __ldg(&sl[k]) - off;  // local
-    const int sx = s % G.nx, yz = s / G.nx, sy = yz % G.ny, sz = yz / G.ny;
-    const uint32_t valid = valid_mask(sx, sy, sz, G);
-    const float hs = h[s];
-    int w[2];
-    bool go[2];
+    uint32_t todo;                       // link slots to walk from
+    if (FROM_REF) {
+      const int yz = div_nx(s, G), sz = div_ny(yz, G);
+      const uint32_t valid = valid_mask(s - yz * G.nx, yz - sz * G.ny, sz, G);
+      const float hs = h[s];
+      uint32_t lower = 0;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int slot = l8 + 8 * j;
-      go[j] = false;
-      w[j] = 0;
-      if (slot < kSlots && (valid & (1u << slot))) {
-        const int u = s + G.delta[slot];
-        const float hu = h[u];
-        const bool lower = (slot < 7) ? (hu <= hs) : (hu < hs);
-        if (lower != SPLIT) {
-          go[j] = true;
-          w[j] = u;
+      for (int q = 0; q < kSlots; ++q)
+        if (valid & (1u << q)) {
+          const float hu = h[s + soff[q]];
+          if ((q < 7) ? (hu <= hs) : (hu < hs)) lower |= 1u << q;
         }
-      }
+      todo = SPLIT ? (valid & ~lower) : lower;
+    } else {
+      const uint32_t m = __ldg(&lm[s]);
+      todo = SPLIT ? (m >> 16) : (m & 0xFFFFu);
     }
-    int e[2] = {0, 0};
-    bool ex[2] = {false, false};  // exits (sharded)
-    bool run[2] = {go[0], go[1]};
-    while (run[0] || run[1]) {
+    int best = -1;
+    float bv = 0.0f;
+    int w[2] = {0, 0};
+    bool run[2] = {false, false};
+    for (;;) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (!run[j] && todo) {
+          w[j] = s + soff[__ffs(todo) - 1];
+          todo &= todo - 1;
+          run[j] = true;
+        }
+      if (!run[0] && !run[1]) break;
       int sv[2];
+      bool ex[2] = {false, false};
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        sv[j] = kSelf;
+        sv[j] = 0;
         if (run[j]) {
-          if (SLAB && (w[j] < lo || w[j] >= hi)) {
-            ex[j] = true;
-            e[j] = w[j];
-            run[j] = false;
-          } else {
-            sv[j] = next_slot<SPLIT, FROM_REF>(w[j], slots, ref);
-          }
+          if (SLAB && (w[j] < lo || w[j] >= hi)) ex[j] = true;
+          else sv[j] = next_slot<SPLIT, FROM_REF>(w[j], slots, ref);
         }
       }
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         if (!run[j]) continue;
-        if (sv[j] == kSelf) {
-          e[j] = w[j];
-          run[j] = false;
-        } else {
-          const int b = slot_bits(sv[j]);
-          w[j] += slot_sign(sv[j]) * ((b & 1) + ((b >> 1) & 1) * G.nx + (b >> 2) * A);
+        if (!ex[j] && sv[j] != kSelf) {
+          w[j] += soff[sv[j]];
+          continue;
         }
+        // a root (or, sharded, the exit into a neighbour's slab)
+        run[j] = false;
+        int lab;
+        float val;
+        if (!SLAB || !ex[j]) {
+          lab = w[j] + off;
+          val = h[w[j]];
+        } else {
+          const int2 t = table_entry(S, w[j] + off, A);
+          lab = t.x;
+          val = __int_as_float(t.y);
+        }
+        bool take;
+        if (best < 0) take = true;
+        else if (!SPLIT) take = (bv < val) || (bv == val && best < lab);  // SoS max
+        else take = (val < bv) || (val == bv && lab < best);               // SoS min
+        if (take) { best = lab; bv = val; }
       }
     }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      if (!go[j]) continue;
-      int lab;
-      float val;
-      if (!SLAB || !ex[j]) {
-        lab = e[j] + off;
-        val = h[e[j]];
-      } else {
-        const int2 t = table_entry(S, e[j] + off, A);
-        lab = t.x;
-        val = __int_as_float(t.y);
-      }
-      bool take;
-      if (best < 0) take = true;
-      else if (!SPLIT) take = (bv < val) || (bv == val && best < lab);
-      else take = (val < bv) || (val == bv && lab < best);
-      if (take) { best = lab; bv = val; }
-    }
-  }
-#pragma unroll
-  for (int o = 4; o >= 1; o >>= 1) {
-    int ob = __shfl_xor_sync(gmask, best, o);
-    float ov = __shfl_xor_sync(gmask, bv, o);
-    bool take;
-    if (ob < 0) take = false;
-    else if (best < 0) take = true;
-    else if (!SPLIT) take = (bv < ov) || (bv == ov && best < ob);  // SoS max
-    else take = (ov < bv) || (ov == bv && ob < best);               // SoS min
-    if (take) { best = ob; bv = ov; }
-  }
-  unsigned hit = 0;
-  if (active && l8 == 0) {
     if (FROM_REF) {
       ref_ext[k] = best;
     } else {
@@ -911,27 +1136,12 @@ __device__ __forceinline__ unsigned events_group8(
       if (best >= 0 && best != want) {
         const int target = SPLIT ? want : best;
         const int t = target - off;
-        if (!SLAB || (t >= G.zb * A && t < G.ze * A)) mark_vertex(marks, t, G);
+        if (!SLAB || (t >= lo && t < hi)) mark_vertex(marks, t, G);
         else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = target;
         hit = 1;
       }
     }
   }
-  return hit;
-}
-
-// one 8-lane group per saddle of sl[0..n)
-template <bool SPLIT, bool FROM_REF, bool SLAB>
-__global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
-                                                const int32_t *__restrict__ sl, int n,
-                                                const uint8_t *__restrict__ slots,
-                                                const uint32_t *__restrict__ ref,
-                                                int32_t *ref_ext, uint32_t *marks, GridP G,
-                                                Slabs S, int32_t *remote,
-                                                unsigned long long *cnt) {
-  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-  const unsigned hit = events_group8<SPLIT, FROM_REF, SLAB>(k, k < n, h, sl, slots, ref, ref_ext,
-                                                            marks, G, S, remote, cnt);
   if (!FROM_REF) warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
 }
 
@@ -995,6 +1205,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
                                                        const int *__restrict__ todo,
                                                        const int *__restrict__ ntodo,
                                                        const uint8_t *__restrict__ slots,
+                                                       const uint32_t *__restrict__ lm,
                                                        int32_t *ref_ext, uint32_t *marks,
                                                        GridP G, EvCache EC, Track T,
                                                        unsigned long long *cnt) {
@@ -1006,7 +1217,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
     const int g = g0 + ((threadIdx.x >> 4) & 1);
     const bool active = g < n;
     const int k = active ? todo[g] : 0;
-    hit += events_group<SPLIT, false, true, false>(k, active, h, sl, slots, nullptr, ref_ext,
+    hit += events_group<SPLIT, false, true, false>(k, active, h, sl, slots, lm, nullptr, ref_ext,
                                                    marks, G, Slabs{nullptr, 1, nullptr},
                                                    nullptr, EC, T, cnt);
   }
@@ -1064,18 +1275,19 @@ __global__ void k_add_offset(int32_t *ids, int n, int off) {
 }
 
 // ---------------------------------------------------- count + edit (O9)
-// Warp-per-word: lanes of a warp cover the 32 vertices of one mark word (one
-// row segment), a persistent grid strides over the words, 4 words in flight
-// per warp.  V_t = popcount of the words; for each marked i not at
-// lo = RU(f_i - xi): a step of Delta (clamped at lo) while c_i < N, else the
-// lossless clamp; c_i++.  Words are cleared for the next round.
-__device__ __forceinline__ void edit_vertex(float *__restrict__ g, uint8_t *__restrict__ c,
+// Eight threads per mark word (one row segment of 32 vertices), four vertices
+// each: a streaming pass over the bitmap in which every marked vertex's f, g,
+// c are loaded independently (coalesced across the warp, no serial chain).
+// V_t = popcount of the words; for each marked i not at lo = RU(f_i - xi): a
+// step of Delta (clamped at lo) while c_i < N, else the lossless clamp;
+// c_i++.  Words are cleared for the next round.
+__device__ __forceinline__ bool edit_vertex(float *__restrict__ g, uint8_t *__restrict__ c,
                                             const float *__restrict__ f, size_t i, float xi,
-                                            float delta, int N, unsigned &ap) {
-  float lo = __fsub_ru(f[i], xi);
-  float gi = g[i];
-  if (gi == lo) return;
-  int ci = c[i];
+                                            float delta, int N) {
+  const float lo = __fsub_ru(f[i], xi);
+  const float gi = g[i];
+  const int ci = c[i];
+  if (gi == lo) return false;
   float t;
   if (ci < N) {
     t = __fsub_rn(gi, delta);
@@ -1085,7 +1297,7 @@ __device__ __forceinline__ void edit_vertex(float *__restrict__ g, uint8_t *__re
   }
   g[i] = t;
   c[i] = (uint8_t)(ci + 1);
-  ++ap;
+  return true;
 }
 
 template <bool TRACK>
@@ -1095,49 +1307,64 @@ __global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
                                                     const float *__restrict__ f, GridP G,
                                                     float xi, float delta, int N, int do_edit,
                                                     Track T, unsigned long long *cnt) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+  const unsigned gmask = 0xffu << (lane & 24);  // the 8 lanes of a word
   const int64_t nwords = (int64_t)G.ny * G.ze * G.W;  // owned rows: [zb*ny, ze*ny)
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned vt = 0, ap = 0;
   for (int64_t w0 = (int64_t)G.ny * G.zb * G.W +
                     (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
        w0 < nwords; w0 += nwarps * 32) {
-    // 32 words per warp step (one per lane, coalesced); only non-zero words
-    // are visited, all lanes together
+    // 32 words per warp step (one per lane, coalesced, cleared); the non-zero
+    // ones are edited four at a time, 8 lanes x 4 vertices per word
     const uint32_t mine = (w0 + lane < nwords) ? marks[w0 + lane] : 0u;
     if (mine) {
       vt += __popc(mine);
       marks[w0 + lane] = 0u;
     }
-    for (uint32_t nzw = __ballot_sync(0xffffffffu, mine != 0u); nzw; nzw &= nzw - 1) {
-      const int j = __ffs(nzw) - 1;
+    uint32_t nzw = __ballot_sync(0xffffffffu, mine != 0u);
+    while (nzw) {
+      // the grp-th remaining non-zero word (if any) goes to lanes 8 grp .. 8 grp + 7
+      uint32_t m = nzw;
+      for (int k = 0; k < grp && m; ++k) m &= m - 1;
+      const int j = m ? __ffs(m) - 1 : 0;
       const uint32_t word = __shfl_sync(0xffffffffu, mine, j);
+      for (int k = 0; k < 4 && nzw; ++k) nzw &= nzw - 1;
+      if (!m) continue;  // uniform over the 8 lanes of the group
       const int64_t w = w0 + j;
       const int64_t row = w / G.W;
-      const unsigned ap0 = ap;
-      if (do_edit && ((word >> lane) & 1u)) {
-        const int x = (int)(w - row * G.W) * 32 + lane;
-        edit_vertex(g, c, f, (size_t)x + (size_t)G.nx * row, xi, delta, N, ap);
+      const int wx = (int)(w - row * G.W);
+      const uint32_t bits = (word >> (4 * sub)) & 15u;
+      const size_t base = (size_t)G.nx * row + (size_t)wx * 32 + 4 * sub;
+      uint32_t e = 0;  // edited vertices of this word (bit = x - 32 wx)
+      if (do_edit) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if ((bits >> q) & 1u)
+            if (edit_vertex(g, c, f, base + q, xi, delta, N)) e |= 1u << (4 * sub + q);
       }
+      ap += __popc(e);
       if (TRACK && (T.bval || T.act_next)) {
-        const uint32_t E = __ballot_sync(0xffffffffu, ap != ap0);  // edited lanes
+        uint32_t E = e;  // OR over the 8 lanes of the word
+        E |= __shfl_xor_sync(gmask, E, 1);
+        E |= __shfl_xor_sync(gmask, E, 2);
+        E |= __shfl_xor_sync(gmask, E, 4);
         if (E) {
-          const int wx = (int)(w - row * G.W), y = (int)(row % G.ny), z = (int)(row / G.ny);
-          if (T.bval && lane == 0)
+          const int y = (int)(row % G.ny), z = (int)(row / G.ny);
+          if (T.bval && sub == 0)
             stamp(T.bval, T.sbval, T, wx, y / BY, z / BZ, (uint16_t)(T.round + 1));
-          if (T.act_next && lane < 7) {
+          if (T.act_next && sub < 7) {
             // closed stars of the edited vertices: 7 (dz, dy) rows, x-1 / x+1
             // spill into the neighbouring words
-            const int dz = lane < 2 ? -1 : (lane < 5 ? 0 : 1);
-            const int dy = (lane == 0 || lane == 2) ? -1 : ((lane == 4 || lane == 6) ? 1 : 0);
-            const bool neg = lane <= 3, pos = lane >= 3;  // x-1 for lanes 0..3, x+1 for 3..6
+            const int dz = kr_dz(sub), dy = kr_dy(sub);
+            const bool neg = sub <= 3, pos = sub >= 3;  // x-1 for rows 0..3, x+1 for 3..6
             const int yy = y + dy, zz = z + dz;
             if (yy >= 0 && yy < G.ny && zz >= 0 && zz < G.nz) {
               uint32_t *r = T.act_next + (size_t)(yy + G.ny * zz) * G.W;
               const int rem = G.nx - wx * 32;  // vertices of this row in the word
               const uint32_t valid = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
-              const uint32_t m = (E | (neg ? (E >> 1) : 0u) | (pos ? (E << 1) : 0u)) & valid;
-              atomicOr(&r[wx], m);
+              const uint32_t mm = (E | (neg ? (E >> 1) : 0u) | (pos ? (E << 1) : 0u)) & valid;
+              atomicOr(&r[wx], mm);
               if (neg && (E & 1u) && wx > 0) atomicOr(&r[wx - 1], 0x80000000u);
               if (pos && (E >> 31) && wx + 1 < G.W) atomicOr(&r[wx + 1], 1u);
             }

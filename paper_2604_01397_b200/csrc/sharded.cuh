@@ -161,6 +161,7 @@ struct Slab {
   float *f = nullptr, *g = nullptr;
   uint32_t *ref = nullptr, *marks = nullptr, *ghost_lo = nullptr, *ghost_hi = nullptr;
   uint8_t *slots = nullptr, *c = nullptr;
+  uint32_t *lm = nullptr;  // g-lower | g-upper << 16 link masks at the f-saddles (stencil -> C3 events)
   uint64_t *keys = nullptr, *allkeys = nullptr, *sorted = nullptr;
   int32_t *S = nullptr, *J = nullptr, *P = nullptr, *m1 = nullptr, *M1 = nullptr;
   int nJ = 0, nP = 0;
@@ -247,6 +248,7 @@ struct ShardedRun {
       G.nz = x.nzl + 2;
       G.V = nx * ny * G.nz;
       G.W = (nx + 31) / 32;
+      grid_fastdiv(G);
       for (int k = 0; k < kSlots; ++k)
         G.delta[k] = kOff[k][0] + nx * (kOff[k][1] + ny * kOff[k][2]);
       G.zoff = x.z0 - 1;
@@ -261,6 +263,7 @@ struct ShardedRun {
       x.g = A.get<float>(Vl);
       x.ref = A.get<uint32_t>(Vl);
       x.slots = A.get<uint8_t>(Vl);
+      x.lm = A.get<uint32_t>(Vl);
       x.c = A.get<uint8_t>(Vl);
       x.marks = A.get<uint32_t>((size_t)G.nz * x.words_per_plane());
       x.ghost_lo = A.get<uint32_t>(x.words_per_plane());
@@ -479,9 +482,10 @@ struct ShardedRun {
   template <bool SPLIT, bool FROM_REF>
   void events(Slab &x, const float *h, const int32_t *list, int n, int32_t *ext) {
     if (n <= 0) return;
-    const int64_t threads = (int64_t)n * 8;
+    const int64_t threads = n;  // one lane per saddle
     k_events<SPLIT, FROM_REF, true><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-        h, list, n, x.slots, x.ref, ext, x.marks, x.G, slabs_of(SPLIT ? x.tup : x.tdn), x.remote,
+        h, list, n, x.slots, FROM_REF ? nullptr : x.lm, x.ref, ext, x.marks, x.G,
+        slabs_of(SPLIT ? x.tup : x.tdn), x.remote,
         x.cnt);
     CK(cudaGetLastError());
   }
@@ -497,8 +501,8 @@ struct ShardedRun {
     const bool c3 = !(flags & EXACTZ_NO_C3);
     zero_counters();
     each([&](Slab &x) {
-      k_stencil<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.G, x.zc, Track{},
-                                                 x.cnt);
+      k_stencil<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm, x.G,
+                                                        x.zc, Track{}, x.cnt);
     });
     CK(cudaGetLastError());
     if (!(flags & EXACTZ_NO_C2) && nS > 1) {

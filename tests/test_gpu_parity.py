@@ -15,7 +15,7 @@ from synth import fields as S
 pytestmark = pytest.mark.gpu
 
 
-def run_both(E, O, f, g, xi, N=5, flags=0, max_iters=0, mode_alias=False):
+def run_both(E, O, f, g, xi, N=5, flags=0, max_iters=0, mode_alias=False, gpu_flags=0):
     fn, gn = f.numpy(), g.numpy()
     ro = O.correct(fn, gn, xi, N, flags=flags, max_iters=max_iters)
     fd, gd = f.cuda(), g.cuda()
@@ -24,7 +24,7 @@ def run_both(E, O, f, g, xi, N=5, flags=0, max_iters=0, mode_alias=False):
     lmin = torch.empty(V, dtype=torch.int32, device="cuda")
     lmax = torch.empty(V, dtype=torch.int32, device="cuda")
     out = gd if mode_alias else None
-    rg = E.exactz_correct(fd, gd, xi, out=out, N=N, flags=flags, max_iters=max_iters,
+    rg = E.exactz_correct(fd, gd, xi, out=out, N=N, flags=flags | gpu_flags, max_iters=max_iters,
                           edit_counts=c, label_min=lmin, label_max=lmax, stats_cap=100000)
     torch.cuda.synchronize()
     return ro, rg, c.cpu().numpy(), lmin.cpu().numpy(), lmax.cpu().numpy()
@@ -171,13 +171,21 @@ def test_repeat_bit_identical(exactz):
     assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
 
 
+# debug flags of exactz_correct (exactz.cu correct_impl): 0x400 compacted
+# stencil passes from the second pass on (never the sparse one), 0x200 no C3
+# cache, 0x100 no vertex activity
+TRACK_MODES = [0, 0x400, 0x400 | 0x200, 0x100]
+
+
+@pytest.mark.parametrize("mode", TRACK_MODES)
 @pytest.mark.parametrize("cfg,shape", [("C2", (40, 48, 200)), ("C3", (33, 40, 150)),
                                        ("C4", (1, 300, 700))])
-def test_tracking_equals_dense(exactz, cfg, shape):
-    """Change tracking (active tiles + cached C3 results) gives the bits of
-    the dense passes, including every per-pass counter."""
+def test_tracking_equals_dense(exactz, cfg, shape, mode):
+    """Change tracking (vertex activity with the compacted or the sparse
+    stencil, cached C3 results) gives the bits of the dense passes, including
+    every per-pass counter."""
     f, g, xi = S.make(cfg, shape=shape, device="cuda")
-    a = exactz.exactz_correct(f, g, xi, stats_cap=100000)
+    a = exactz.exactz_correct(f, g, xi, flags=mode, stats_cap=100000)
     b = exactz.exactz_correct(f, g, xi, flags=exactz.NO_TRACK, stats_cap=100000)
     assert a.iters == b.iters and a.status == b.status
     assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
@@ -200,3 +208,12 @@ def test_tracking_equals_dense_reformulated(exactz):
                               stats_cap=100000)
     assert a.iters == b.iters and a.stats == b.stats
     assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
+
+
+@pytest.mark.parametrize("cfg,shape", [("C1", None), ("C2", (19, 13, 67)), ("C3", (11, 17, 97)),
+                                       ("C4", (1, 41, 133)), ("C2", (9, 3, 33))])
+def test_parity_compacted_passes(exactz, oracle, cfg, shape):
+    """The compacted stencil (forced from the second pass on) on ragged tiles
+    (nx not a multiple of 32, ny not of 8): bit-exact with the oracle."""
+    f, g, xi = S.make(cfg, shape=shape)
+    assert_parity(*run_both(exactz, oracle, f, g, xi, gpu_flags=0x400))
