@@ -56,8 +56,8 @@ struct GridP {
   int delta[kSlots];  // linear offset of each slot
   int zoff, gnz;      // global z of local plane 0, global nz
   int zb, ze;         // owned local planes [zb, ze)
-  uint32_t mnx, mny;  // division by nx, ny: q = (umulhi(n, m) + n) >> l (n < 2^31)
-  int lnx, lny;
+  uint32_t mnx, mny, mW;  // division by nx, ny, W: q = (umulhi(n, m) + n) >> l (n < 2^31)
+  int lnx, lny, lW;
 };
 
 // Magic numbers of the unsigned division n / d for n < 2^31, d >= 1
@@ -70,12 +70,16 @@ inline void fastdiv_magic(uint32_t d, uint32_t &m, int &l) {
 inline void grid_fastdiv(GridP &G) {
   fastdiv_magic((uint32_t)G.nx, G.mnx, G.lnx);
   fastdiv_magic((uint32_t)G.ny, G.mny, G.lny);
+  fastdiv_magic((uint32_t)G.W, G.mW, G.lW);
 }
 __device__ __forceinline__ int div_nx(int n, const GridP &G) {
   return (int)((__umulhi((uint32_t)n, G.mnx) + (uint32_t)n) >> G.lnx);
 }
 __device__ __forceinline__ int div_ny(int n, const GridP &G) {
   return (int)((__umulhi((uint32_t)n, G.mny) + (uint32_t)n) >> G.lny);
+}
+__device__ __forceinline__ int div_W(int n, const GridP &G) {  // mark-bitmap row of word n
+  return (int)((__umulhi((uint32_t)n, G.mW) + (uint32_t)n) >> G.lW);
 }
 
 // Change tracking (single GPU, late rounds).
@@ -530,20 +534,21 @@ __global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
       const unsigned fired = __ballot_sync(0xffffffffu, tgt != 0);
       if (tx == 0 && fired) atomicOr(&T.act_next[(size_t)(y + G.ny * z) * G.W + bx], fired);
     }
-    // warp-aggregated marks: one ballot per slot, shifted into the 7 row masks
+    // warp-aggregated marks: the targets re-indexed in ascending linear
+    // order (slots 0..6, self, 7..13) put each (dz, dy) row's 2-3 slots on
+    // adjacent bits; per row, lane l contributes those bits shifted to
+    // 1 + dx + l and one OR-reduction per 32-bit half builds the 34-bit row
     u64 rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (__any_sync(0xffffffffu, tgt)) {
-      uint32_t bal[15];
+      const uint32_t t = (tgt & 0x7Fu) | ((tgt & 0x3F80u) << 1) | ((tgt >> kSelf) << 7);
 #pragma unroll
-      for (int s = 0; s < 15; ++s) bal[s] = __ballot_sync(0xffffffffu, tgt & (1u << s));
-      // bit position = 1 + dx (lane 0 <-> lx 1)
-      rv[0] = (u64)bal[0] | ((u64)bal[1] << 1);                        // (-1,-1): slots 0, 1
-      rv[1] = (u64)bal[2] | ((u64)bal[3] << 1);                        // (-1, 0): slots 2, 3
-      rv[2] = (u64)bal[4] | ((u64)bal[5] << 1);                        // ( 0,-1): slots 4, 5
-      rv[3] = (u64)bal[6] | ((u64)bal[14] << 1) | ((u64)bal[7] << 2);  // ( 0, 0): 6, self, 7
-      rv[4] = ((u64)bal[8] << 1) | ((u64)bal[9] << 2);                 // ( 0, 1): slots 8, 9
-      rv[5] = ((u64)bal[10] << 1) | ((u64)bal[11] << 2);               // ( 1, 0): slots 10, 11
-      rv[6] = ((u64)bal[12] << 1) | ((u64)bal[13] << 2);               // ( 1, 1): slots 12, 13
+      for (int k = 0; k < KR; ++k) {
+        constexpr int kStart[KR] = {0, 2, 4, 6, 9, 11, 13};
+        const uint32_t c = ((t >> kStart[k]) & (k == 3 ? 7u : 3u)) << (k >= 4 ? 1 : 0);
+        const uint32_t lo = __reduce_or_sync(0xffffffffu, c << tx);
+        const uint32_t hi = __reduce_or_sync(0xffffffffu, tx >= 30 ? c >> (32 - tx) : 0u);
+        rv[k] = (u64)lo | ((u64)hi << 32);
+      }
     }
     if (tx == 0) {
       ulonglong2 *d = reinterpret_cast<ulonglong2 *>(&wr[z & 3][ty][0]);
@@ -751,8 +756,8 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
     const int j = __ffs(nzw) - 1;
     const uint32_t word = __shfl_sync(0xffffffffu, mine, j);
     const int64_t w = base + j;
-    const int row = (int)(w / G.W), wx = (int)(w - (int64_t)row * G.W);
-    const int y = row % G.ny, z = row / G.ny, x = wx * 32 + lane;
+    const int row = div_W((int)w, G), wx = (int)w - row * G.W;
+    const int z = div_ny(row, G), y = row - z * G.ny, x = wx * 32 + lane;
     uint32_t tgt = 0;
     bool schg = false;
     if (((word >> lane) & 1u) && x < G.nx) {
@@ -1162,7 +1167,7 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
     valid = rnd != 0 && !(mask & kFar);
     if (valid) {
       const int s = sl[k];
-      const int sx = s % G.nx, yz = s / G.nx, sy = yz % G.ny, sz = yz / G.ny;
+      const int yz = div_nx(s, G), sz = div_ny(yz, G), sx = s - yz * G.nx, sy = yz - sz * G.ny;
       const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
       for (uint32_t m = (uint32_t)mask; m && valid; m &= m - 1) {
         const int j = __ffs(m) - 1;
@@ -1197,8 +1202,10 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
   warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
 }
 
-// recompute (and cache) the listed saddles: warps stride over the list, two
-// 16-lane groups per warp
+// Recompute (and cache) the listed saddles, one lane per saddle as in
+// k_events, recording the bricks the result depends on: the saddle's closed
+// star (its link masks come from those values) and every vertex of every walk
+// (a slot change anywhere on a path can move its root).
 template <bool SPLIT>
 __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__ h,
                                                        const int32_t *__restrict__ sl,
@@ -1209,17 +1216,98 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
                                                        int32_t *ref_ext, uint32_t *marks,
                                                        GridP G, EvCache EC, Track T,
                                                        unsigned long long *cnt) {
+  __shared__ int soff[16], sdel[16];  // linear offset; packed (dx+1, dy+1, dz+1)
+  if (threadIdx.x < 16) {
+    const int q = threadIdx.x;
+    soff[q] = q < kSlots ? slot_delta(q, G) : 0;
+    int p = 1 | (1 << 2) | (1 << 4);
+    if (q < kSlots) {
+      const int b = slot_bits(q), sg1 = slot_sign(q);
+      p = (1 + sg1 * (b & 1)) | ((1 + sg1 * ((b >> 1) & 1)) << 2) | ((1 + sg1 * (b >> 2)) << 4);
+    }
+    sdel[q] = p;
+  }
+  __syncthreads();
   const int n = *ntodo;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
   unsigned hit = 0;
-  for (int g0 = warp * 2; g0 < n; g0 += nwarps * 2) {
-    const int g = g0 + ((threadIdx.x >> 4) & 1);
+  if (n * 16 <= (int)(gridDim.x * blockDim.x)) {
+    // few saddles (late passes: mostly long walks that never stay cached):
+    // 16 lanes per saddle, one walk per lane, for the shortest critical path
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
     const bool active = g < n;
-    const int k = active ? todo[g] : 0;
-    hit += events_group<SPLIT, false, true, false>(k, active, h, sl, slots, lm, nullptr, ref_ext,
-                                                   marks, G, Slabs{nullptr, 1, nullptr},
-                                                   nullptr, EC, T, cnt);
+    hit = events_group<SPLIT, false, true, false>(active ? todo[g] : 0, active, h, sl, slots, lm,
+                                                  nullptr, ref_ext, marks, G,
+                                                  Slabs{nullptr, 1, nullptr}, nullptr, EC, T, cnt);
+    warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
+    return;
+  }
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
+    const int k = todo[g];
+    const int s = __ldg(&sl[k]);
+    const int yz = div_nx(s, G), sz = div_ny(yz, G);
+    const int sx = s - yz * G.nx, sy = yz - sz * G.ny;
+    const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
+    const uint32_t m = __ldg(&lm[s]);
+    unsigned long long mask = 0;
+    brick_bit(sx, sy, sz, bsx, bsy, bsz, mask);
+    for (uint32_t v = (m | (m >> 16)) & 0x3FFFu; v; v &= v - 1) {  // the star
+      const int p = sdel[__ffs(v) - 1];
+      brick_bit(sx + (p & 3) - 1, sy + ((p >> 2) & 3) - 1, sz + (p >> 4) - 1, bsx, bsy, bsz, mask);
+    }
+    uint32_t rest = SPLIT ? (m >> 16) : (m & 0xFFFFu);
+    int best = -1;
+    float bv = 0.0f;
+    int w[2] = {0, 0}, x[2] = {0, 0}, y[2] = {0, 0}, z[2] = {0, 0};
+    bool run[2] = {false, false};
+    for (;;) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (!run[j] && rest) {
+          const int q = __ffs(rest) - 1, p = sdel[q];
+          rest &= rest - 1;
+          w[j] = s + soff[q];
+          x[j] = sx + (p & 3) - 1;
+          y[j] = sy + ((p >> 2) & 3) - 1;
+          z[j] = sz + (p >> 4) - 1;
+          run[j] = true;
+        }
+      if (!run[0] && !run[1]) break;
+      int sv[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        sv[j] = run[j] ? (__ldg(&slots[w[j]]) >> (SPLIT ? 4 : 0)) & 15 : 0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (!run[j]) continue;
+        if (sv[j] != kSelf) {
+          const int p = sdel[sv[j]];
+          w[j] += soff[sv[j]];
+          x[j] += (p & 3) - 1;
+          y[j] += ((p >> 2) & 3) - 1;
+          z[j] += (p >> 4) - 1;
+          brick_bit(x[j], y[j], z[j], bsx, bsy, bsz, mask);
+          continue;
+        }
+        run[j] = false;
+        const int lab = w[j];
+        const float val = h[lab];
+        bool take;
+        if (best < 0) take = true;
+        else if (!SPLIT) take = (bv < val) || (bv == val && best < lab);  // SoS max
+        else take = (val < bv) || (val == bv && lab < best);               // SoS min
+        if (take) { best = lab; bv = val; }
+      }
+    }
+    int target = -1;
+    const int want = ref_ext[k];
+    if (best >= 0 && best != want) target = SPLIT ? want : best;
+    EC.rnd[k] = (uint16_t)T.round;
+    EC.mask[k] = mask;
+    EC.tgt[k] = target;
+    if (target >= 0) {
+      mark_vertex(marks, target, G);
+      hit = 1;
+    }
   }
   warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
 }
@@ -1332,7 +1420,7 @@ __global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
       for (int k = 0; k < 4 && nzw; ++k) nzw &= nzw - 1;
       if (!m) continue;  // uniform over the 8 lanes of the group
       const int64_t w = w0 + j;
-      const int64_t row = w / G.W;
+      const int64_t row = div_W((int)w, G);
       const int wx = (int)(w - row * G.W);
       const uint32_t bits = (word >> (4 * sub)) & 15u;
       const size_t base = (size_t)G.nx * row + (size_t)wx * 32 + 4 * sub;
@@ -1350,7 +1438,7 @@ __global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
         E |= __shfl_xor_sync(gmask, E, 2);
         E |= __shfl_xor_sync(gmask, E, 4);
         if (E) {
-          const int y = (int)(row % G.ny), z = (int)(row / G.ny);
+          const int z = div_ny((int)row, G), y = (int)row - z * G.ny;
           if (T.bval && sub == 0)
             stamp(T.bval, T.sbval, T, wx, y / BY, z / BZ, (uint16_t)(T.round + 1));
           if (T.act_next && sub < 7) {
