@@ -207,7 +207,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    from paper_2604_01397_b200 import _build
+    from __graft_entry__ import _load_builder
+    _build = _load_builder()
     if rank == 0:
         _build.build()
     if ws > 1:

@@ -30,7 +30,8 @@ def exactz():
     import torch
     if not torch.cuda.is_available():
         pytest.fail("gpu test collected without a CUDA device")
-    from paper_2604_01397_b200 import _build
+    from __graft_entry__ import _load_builder
+    _build = _load_builder()
     _build.build()
     import paper_2604_01397_b200 as E
     return E

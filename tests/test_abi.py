@@ -15,7 +15,8 @@ def declared_functions():
 
 
 def test_library_exports_every_declared_symbol():
-    from paper_2604_01397_b200 import _build
+    from __graft_entry__ import _load_builder
+    _build = _load_builder()
     lib_path = _build.build()
     lib = ctypes.CDLL(lib_path)
     names = declared_functions()
@@ -28,7 +29,8 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_cubin_is_sm100a():
-    from paper_2604_01397_b200 import _build
+    from __graft_entry__ import _load_builder
+    _build = _load_builder()
     lib_path = _build.build()
     out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib_path],
                                   text=True)
