@@ -20,6 +20,7 @@
 
 #include "../../include/exactz.h"
 #include "kernels.cuh"
+#include "stencil_fast.cuh"
 
 #ifndef EXACTZ_GIT
 #define EXACTZ_GIT "dev"
@@ -145,6 +146,7 @@ struct Ctx {
   dim3 sgrid, sblock;                 // stencil: 32x8 columns, z chunks
   dim3 rgrid, vblock;                 // persistent row-parallel grid, 128 x-threads
   int zc = 1;
+  bool fast = false;                  // every lo >= 0: k_stencil_fast (set by validation)
   unsigned long long *cnt = nullptr;  // device counters
   unsigned long long *hcnt = nullptr; // pinned host mirror
   Arena arena;
@@ -351,18 +353,21 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
   // S: all saddles sorted by the SoS key of f.  J, P: join / split
   // saddles in index (spatial) order, so that consecutive event checks walk
   // nearby integral paths (L1/L2 reuse); their order is otherwise irrelevant.
+  // They are selected from the saddle ids sorted by index (Sx).
   uint64_t *sorted = C.arena.get<uint64_t>(R.nS);
   R.S = C.arena.get<int32_t>(R.nS);
   R.J = C.arena.get<int32_t>(R.nS);
   R.P = C.arena.get<int32_t>(R.nS);
+  int32_t *Sx = C.arena.get<int32_t>(R.nS);
   int *nsel = C.arena.get<int>(2);
   if (R.nS > 0) {
-    size_t tb = 0, tb2 = 0, tb3 = 0;
-    cub::CountingInputIterator<int32_t> ids(0);
+    size_t tb = 0, tb1 = 0, tb2 = 0, tb3 = 0;
     CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, R.nS, 0, 64, C.s));
-    CK(cub::DeviceSelect::If(nullptr, tb2, ids, R.J, nsel, (int)V, IsJoin{R.ref}, C.s));
-    CK(cub::DeviceSelect::If(nullptr, tb3, ids, R.P, nsel + 1, (int)V, IsSplit{R.ref}, C.s));
-    size_t tmax = tb > tb2 ? tb : tb2;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tb1, R.S, Sx, R.nS, 0, 32, C.s));
+    CK(cub::DeviceSelect::If(nullptr, tb2, Sx, R.J, nsel, R.nS, IsJoin{R.ref}, C.s));
+    CK(cub::DeviceSelect::If(nullptr, tb3, Sx, R.P, nsel + 1, R.nS, IsSplit{R.ref}, C.s));
+    size_t tmax = tb > tb1 ? tb : tb1;
+    tmax = tmax > tb2 ? tmax : tb2;
     tmax = tmax > tb3 ? tmax : tb3;
     void *tmp = C.arena.get<uint8_t>(tmax);
     C.run(EXACTZ_K_REFERENCE, 32ull * R.nS, false, [&] {
@@ -371,9 +376,10 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
     C.run(EXACTZ_K_REFERENCE, 12ull * R.nS, true, [&] {
       k_keys_to_ids<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(sorted, R.S, R.nS);
     });
-    C.run(EXACTZ_K_REFERENCE, 8ull * V, false, [&] {
-      CK(cub::DeviceSelect::If(tmp, tb2, ids, R.J, nsel, (int)V, IsJoin{R.ref}, C.s));
-      CK(cub::DeviceSelect::If(tmp, tb3, ids, R.P, nsel + 1, (int)V, IsSplit{R.ref}, C.s));
+    C.run(EXACTZ_K_REFERENCE, 16ull * R.nS, false, [&] {
+      CK(cub::DeviceRadixSort::SortKeys(tmp, tb1, R.S, Sx, R.nS, 0, 32, C.s));
+      CK(cub::DeviceSelect::If(tmp, tb2, Sx, R.J, nsel, R.nS, IsJoin{R.ref}, C.s));
+      CK(cub::DeviceSelect::If(tmp, tb3, Sx, R.P, nsel + 1, R.nS, IsSplit{R.ref}, C.s));
     });
     int h[2];
     CK(cudaMemcpyAsync(h, nsel, sizeof(h), cudaMemcpyDeviceToHost, C.s));
@@ -404,6 +410,8 @@ struct Tracking {
   bool sparse = false;  // few active vertices: the sparse stencil, else the compacted one
   uint32_t *act[2] = {nullptr, nullptr};
   int cur = 0;
+  int32_t *list = nullptr;  // active vertices of a sparse pass (k_act_list)
+  int *nlist = nullptr;
   // C3 cache with brick stamps
   bool cache_on = false;
   int nbx = 0, nby = 0, nbz = 0, nb = 0, nsx = 0, nsy = 0, nsz = 0, nsb = 0;
@@ -425,6 +433,8 @@ struct Tracking {
       act[k] = C.arena.get<uint32_t>(C.mark_words());
       CK(cudaMemsetAsync(act[k], 0, C.mark_words() * 4, C.s));
     }
+    list = C.arena.get<int32_t>((size_t)C.V);
+    nlist = C.arena.get<int>(1);
     act_on = true;
   }
   void start_cache(Ctx &C, const Reference &R) {
@@ -483,6 +493,17 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
   const Track T = trk ? trk->track(round) : Track{};
   const bool sparse = trk && trk->ready && trk->sparse;
   const bool compact = trk && trk->ready && !trk->sparse;
+  // R4 (C2) needs only the snapshot g: it runs on side stream 1 concurrently
+  // with the stencil
+  C.fork();
+  C.on_side(1);
+  if (!(flags & EXACTZ_NO_C2) && R.nS > 1) {
+    C.run(EXACTZ_K_SADDLE_ORDER, 8ull * R.nS, true, [&] {
+      k_saddle_order<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(g, R.S, R.nS, marks, C.G,
+                                                                      C.cnt);
+    });
+  }
+  C.s = C.main_s;
   // algorithmic bytes per vertex: g 4 + ref 4 read, slots 1 + mark bits 1/8
   // written; a sparse or compacted pass: the active vertices
   // only (plus the activity bitmap)
@@ -493,7 +514,16 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
     });
   } else if (!sparse) {
     C.run(EXACTZ_K_STENCIL, (uint64_t)C.V * 73 / 8, true, [&] {
-      if (trk)
+      if (C.fast && trk)
+        k_stencil_fast<true><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G, C.zc,
+                                                            T, C.cnt);
+      else if (C.fast && (flags & 0x1000u))  // experiment: ALU-pipe lower mask
+        k_stencil_fast<false, true><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm,
+                                                                   C.G, C.zc, T, C.cnt);
+      else if (C.fast)
+        k_stencil_fast<false><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G,
+                                                             C.zc, T, C.cnt);
+      else if (trk)
         k_stencil<true><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G, C.zc, T,
                                                        C.cnt);
       else
@@ -501,22 +531,21 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
                                                         C.cnt);
     });
   } else {
+    CK(cudaMemsetAsync(trk->nlist, 0, sizeof(int), C.s));
     C.run(EXACTZ_K_SPARSE, (uint64_t)C.V / 8, true, [&] {
-      k_stencil_sparse<<<148 * 8, 256, 0, C.s>>>(g, R.ref, marks, slots, lm, trk->act[trk->cur],
-                                                 C.G, T, C.cnt);
+      k_act_list<<<148 * 16, 256, 0, C.s>>>(trk->act[trk->cur], C.G, trk->list, trk->nlist);
+    });
+    C.run(EXACTZ_K_SPARSE, 0, true, [&] {
+      k_stencil_list<<<148 * 16, 256, 0, C.s>>>(g, R.ref, marks, slots, lm, trk->list,
+                                                trk->nlist, C.G, T, C.cnt);
     });
   }
-  // R4 and the two C3 event kernels are independent (all read the snapshot g
-  // and the slots, all only OR marks and add counters): run them on two side
+  // R4 (launched before the stencil on side stream 1) and the two C3 event
+  // kernels are independent (all read the snapshot g and the stencil's slots,
+  // all only OR marks and add counters): the events run on the two side
   // streams, joined before the count/edit.
   C.fork();
   C.on_side(1);
-  if (!(flags & EXACTZ_NO_C2) && R.nS > 1) {
-    C.run(EXACTZ_K_SADDLE_ORDER, 8ull * R.nS, true, [&] {
-      k_saddle_order<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(g, R.S, R.nS, marks, C.G,
-                                                                      C.cnt);
-    });
-  }
   if (c3 && (flags & EXACTZ_REFORMULATED) && R.nC > 1) {
     // R7: adjacent critical points in the f order
     C.run(EXACTZ_K_EVENTS, 8ull * R.nC, true, [&] {
@@ -557,11 +586,14 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
   return o;
 }
 
-static void validate_inputs(Ctx &C, const float *f, const float *g, float xi) {
+static void validate_inputs(Ctx &C, const float *f, const float *g, float xi,
+                            uint32_t flags = 0) {
   C.zero();
   C.run(EXACTZ_K_VALIDATE, 8 * (uint64_t)C.V, true,
         [&] { k_validate<<<blocks_for(C.V, 256), 256, 0, C.s>>>(f, g, C.V, xi, C.cnt); });
   C.read();
+  // debug flag 0x800: the general stencil even for non-negative fields
+  C.fast = C.hcnt[C_NEG] == 0 && !(flags & 0x800u);
   if (C.hcnt[C_BAD_NF]) {
     set_err("validate", "non-finite value in f or g");
     throw Error{EXACTZ_EINVAL};
@@ -594,7 +626,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   CK(cudaEventCreate(&e1));
   CK(cudaEventCreate(&e2));
   CK(cudaEventRecord(e0, s));
-  validate_inputs(C, f, g_in, eps);
+  validate_inputs(C, f, g_in, eps, flags);
   if (out != g_in) CK(cudaMemcpyAsync(out, g_in, V * sizeof(float), cudaMemcpyDeviceToDevice, s));
   Reference R;
   build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
@@ -612,16 +644,16 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   Tracking trk;
   trk.geometry(C);
   static const unsigned long long act_div = [] {
-    const char *e = std::getenv("EXACTZ_ACT_DIV");  // tuning knob (default 1024)
-    return e ? std::strtoull(e, nullptr, 10) : 1024ull;
+    const char *e = std::getenv("EXACTZ_ACT_DIV");  // tuning knob (default 64)
+    return e ? std::strtoull(e, nullptr, 10) : 64ull;
   }();
   static const unsigned long long cache_div = [] {
     const char *e = std::getenv("EXACTZ_CACHE_DIV");  // tuning knob (default 4)
     return e ? std::strtoull(e, nullptr, 10) : 4ull;
   }();
   static const unsigned long long compact_div = [] {
-    const char *e = std::getenv("EXACTZ_COMPACT_DIV");  // tuning knob (default 32)
-    return e ? std::strtoull(e, nullptr, 10) : 32ull;
+    const char *e = std::getenv("EXACTZ_COMPACT_DIV");  // tuning knob (default 0: off)
+    return e ? std::strtoull(e, nullptr, 10) : 0ull;
   }();
   unsigned long long prev_vt = (unsigned long long)V;
   const bool allow_track = !(flags & EXACTZ_NO_TRACK);
@@ -629,15 +661,16 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     bool may_edit = !(max_iters && it >= max_iters);
     const int round = (int)rows + 1;  // stamps are 16-bit pass numbers
     if (allow_track && rows >= 1 && round < 65000) {
-      // vertex activity once < V/compact_div vertices are marked (compacted
-      // dense passes; the sparse stencil below V/act_div); the C3 cache once
-      // the marks are sparse at brick scale
-      // (debug flag 0x400: compacted passes from the second pass on, never
-      // the sparse stencil)
+      // vertex activity once <= V/act_div vertices are marked: the pass after
+      // uses the list-based sparse stencil; the C3 cache once the marks are
+      // sparse at brick scale
+      // (debug flag 0x400: compacted passes from the second pass on instead
+      // of the list-based ones)
       const bool force_compact = (flags & 0x400u) != 0;
-      trk.sparse = !force_compact && prev_vt * act_div <= (unsigned long long)V;
+      trk.sparse = !force_compact;
       if (!(flags & 0x100u) && !trk.act_on &&
-          (force_compact || trk.sparse || prev_vt * compact_div <= (unsigned long long)V))
+          (force_compact || prev_vt * act_div <= (unsigned long long)V ||
+           (compact_div && prev_vt * compact_div <= (unsigned long long)V)))
         trk.start_act(C);
       if (!(flags & (0x200u | EXACTZ_REFORMULATED)) && !trk.cache_on &&
           prev_vt * cache_div <= (unsigned long long)trk.nb)
@@ -765,7 +798,7 @@ exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3]
     Ctx C(s);
     C.V = V;
     C.init(dims);
-    validate_inputs(C, f, g, eps_abs);
+    validate_inputs(C, f, g, eps_abs, flags);
     Reference R;
     build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
     uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());

@@ -43,7 +43,8 @@ enum Counter {
   C_NREMOTE = 14,  // sharded: remote marks appended by k_events
   C_WALK = 15,     // diagnostic: steps taken by the label walks of a pass
   C_NCP = 8,       // reference: critical points (shares the slot of C_CHANGED)
-  C_NCOUNTERS = 16
+  C_NEG = 16,      // validation: lo = RU(f - xi) < 0 or g = -0.0 (k_stencil_fast needs none)
+  C_NCOUNTERS = 18
 };
 
 // Geometry of the (local) grid a kernel works on.  Single GPU: the whole
@@ -269,7 +270,7 @@ __device__ __forceinline__ bool sos_less_g(const float *h, int u, int v) {
 // ---------------------------------------------------------------- validate (O1)
 __global__ void k_validate(const float *__restrict__ f, const float *__restrict__ g, int64_t V,
                            float xi, unsigned long long *cnt) {
-  unsigned nf = 0, nb = 0;
+  unsigned nf = 0, nb = 0, ng = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V;
        i += (int64_t)gridDim.x * blockDim.x) {
     float a = f[i], b = g[i];
@@ -279,9 +280,11 @@ __global__ void k_validate(const float *__restrict__ f, const float *__restrict_
     }
     float lo = __fsub_ru(a, xi), hi = __fadd_rd(a, xi);
     if (!(lo <= b && b <= hi)) ++nb;
+    if (lo < 0.0f || __float_as_uint(b) == 0x80000000u) ++ng;  // -0.0 in g: general stencil
   }
   warp_add(&cnt[C_BAD_NF], nf);
   warp_add(&cnt[C_BAD_BOUND], nb);
+  warp_add(&cnt[C_NEG], ng);
 }
 
 // ------------------------------------------------------ reference of f (O7)
@@ -291,26 +294,39 @@ __device__ __forceinline__ void reference_vertex(const float *__restrict__ f, co
                                                  uint32_t *__restrict__ ref,
                                                  uint64_t *saddle_keys, uint64_t *cp_keys,
                                                  unsigned long long *cnt, int x, int y, int z) {
-  int i = x + G.nx * (y + G.ny * z);
-  uint32_t valid = valid_mask(x, y, z, G);
-  Star st = eval_star(f, i, valid, G);
-  int nlc, nuc;
-  link_type(st.lower, valid, nlc, nuc);
-  bool isext = (nlc == 0) || (nuc == 0);
-  bool sad = !isext && (nlc >= 2 || nuc >= 2);
-  bool join = sad && nlc >= 2, split = sad && nuc >= 2;
-  ref[i] = st.lower | ((uint32_t)st.dn << 14) | ((uint32_t)st.up << 18) | ((uint32_t)nlc << 22) |
-           ((uint32_t)nuc << 25) | ((uint32_t)sad << 28) | ((uint32_t)join << 29) |
-           ((uint32_t)split << 30);
-  const uint32_t ig = (uint32_t)(i + G.zoff * G.nx * G.ny);  // global index (SoS)
-  if (sad) {
-    unsigned long long k = atomicAdd(&cnt[C_NSADDLE], 1ull);
-    saddle_keys[k] = ((uint64_t)ordered_key(f[i]) << 32) | ig;
+  const bool in = x < G.nx;  // lanes past the row end take part in the ballots only
+  const int i = in ? x + G.nx * (y + G.ny * z) : 0;
+  bool isext = false, sad = false;
+  uint64_t key = 0;
+  if (in) {
+    uint32_t valid = valid_mask(x, y, z, G);
+    Star st = eval_star(f, i, valid, G);
+    int nlc, nuc;
+    link_type(st.lower, valid, nlc, nuc);
+    isext = (nlc == 0) || (nuc == 0);
+    sad = !isext && (nlc >= 2 || nuc >= 2);
+    const bool join = sad && nlc >= 2, split = sad && nuc >= 2;
+    ref[i] = st.lower | ((uint32_t)st.dn << 14) | ((uint32_t)st.up << 18) |
+             ((uint32_t)nlc << 22) | ((uint32_t)nuc << 25) | ((uint32_t)sad << 28) |
+             ((uint32_t)join << 29) | ((uint32_t)split << 30);
+    const uint32_t ig = (uint32_t)(i + G.zoff * G.nx * G.ny);  // global index (SoS)
+    key = ((uint64_t)ordered_key(f[i]) << 32) | ig;
   }
-  if (cp_keys && (sad || isext)) {  // every critical point (reformulation)
-    unsigned long long k = atomicAdd(&cnt[C_NCP], 1ull);
-    cp_keys[k] = ((uint64_t)ordered_key(f[i]) << 32) | ig;
+  // warp-aggregated appends (one atomic per warp and list; list order is
+  // irrelevant: the keys are sorted afterwards)
+  const unsigned ms = __ballot_sync(0xffffffffu, sad);
+  const unsigned mc = cp_keys ? __ballot_sync(0xffffffffu, sad || isext) : 0u;
+  const int lane = threadIdx.x & 31;
+  unsigned long long bs = 0, bc = 0;
+  if (lane == 0) {
+    if (ms) bs = atomicAdd(&cnt[C_NSADDLE], (unsigned long long)__popc(ms));
+    if (mc) bc = atomicAdd(&cnt[C_NCP], (unsigned long long)__popc(mc));
   }
+  const unsigned below = (1u << lane) - 1u;
+  bs = __shfl_sync(0xffffffffu, bs, 0);
+  bc = __shfl_sync(0xffffffffu, bc, 0);
+  if (sad) saddle_keys[bs + __popc(ms & below)] = key;
+  if (cp_keys && (sad || isext)) cp_keys[bc + __popc(mc & below)] = key;
 }
 
 // Persistent 2D grid over rows (y + ny*z) and x.
@@ -318,9 +334,12 @@ __global__ void __launch_bounds__(128) k_reference(const float *__restrict__ f, 
                                                    uint32_t *__restrict__ ref,
                                                    uint64_t *saddle_keys, uint64_t *cp_keys,
                                                    unsigned long long *cnt) {
+  // warp-uniform trip counts (the appends use warp ballots); lanes past nx idle
   for (int row = G.zb * G.ny + blockIdx.y; row < G.ze * G.ny; row += gridDim.y)
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < G.nx; x += gridDim.x * blockDim.x)
-      reference_vertex(f, G, ref, saddle_keys, cp_keys, cnt, x, row % G.ny, row / G.ny);
+    for (int xb = blockIdx.x * blockDim.x + (threadIdx.x & ~31); xb < G.nx;
+         xb += gridDim.x * blockDim.x)
+      reference_vertex(f, G, ref, saddle_keys, cp_keys, cnt, xb + (threadIdx.x & 31), row % G.ny,
+                       row / G.ny);
 }
 
 __global__ void k_keys_to_ids(const uint64_t *__restrict__ keys, int32_t *ids, int n) {
@@ -797,6 +816,106 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
       if (lane == 0 && fired) atomicOr(&T.act_next[w], fired);
     }
    }
+  }
+  warp_add(&cnt[C_N1 + 0], n1);
+  warp_add(&cnt[C_N1 + 1], n2);
+  warp_add(&cnt[C_N1 + 2], n3);
+}
+
+// List-based sparse pass (tracking): k_act_list compacts the activity bitmap
+// into a list of vertex indices (words consumed and cleared), then
+// k_stencil_list evaluates one listed vertex per thread (full parallelism;
+// the neighbours come from global memory, mostly L1/L2 hits).  Same rules and
+// outputs as k_stencil_sparse.
+__global__ void __launch_bounds__(256) k_act_list(uint32_t *__restrict__ act, GridP G,
+                                                  int32_t *__restrict__ list, int *count) {
+  __shared__ int wsum[8], bbase;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t w0 = (int64_t)G.ny * G.zb * G.W, nwords = (int64_t)G.ny * G.ze * G.W;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = w0 + (int64_t)blockIdx.x * blockDim.x; base < nwords;
+       base += stride) {  // block-uniform trip count
+    const int64_t w = base + threadIdx.x;
+    uint32_t a = 0;
+    int row = 0, x0 = 0;
+    if (w < nwords) {
+      a = act[w];
+      if (a) {
+        act[w] = 0u;
+        row = div_W((int)w, G);
+        x0 = ((int)w - row * G.W) * 32;
+        if (G.nx - x0 < 32) a &= (1u << (G.nx - x0)) - 1u;
+      }
+    }
+    const int n = __popc(a);
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // one atomic per block and step
+      int tot = 0;
+      for (int k = 0; k < 8; ++k) {
+        const int v = wsum[k];
+        wsum[k] = tot;
+        tot += v;
+      }
+      bbase = tot ? atomicAdd(count, tot) : 0;
+    }
+    __syncthreads();
+    int k = bbase + wsum[warp] + incl - n;
+    const int i0 = row * G.nx + x0;
+    for (; a; a &= a - 1) list[k++] = i0 + __ffs(a) - 1;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_stencil_list(const float *__restrict__ g,
+                                                      const uint32_t *__restrict__ ref,
+                                                      uint32_t *__restrict__ marks,
+                                                      uint8_t *__restrict__ slots,
+                                                      uint32_t *__restrict__ lm,
+                                                      const int32_t *__restrict__ list,
+                                                      const int *__restrict__ count, GridP G,
+                                                      Track T, unsigned long long *cnt) {
+  const int n = *count;
+  unsigned n1 = 0, n2 = 0, n3 = 0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int i = __ldg(&list[k]);
+    const int row = div_nx(i, G), x = i - row * G.nx;
+    const int z = div_ny(row, G), y = row - z * G.ny;
+    const uint32_t valid = valid_mask(x, y, z, G);
+    const Star st = eval_star(g, i, valid, G);
+    const uint32_t r = __ldg(&ref[i]);
+    uint32_t tgt = 0;
+    if (st.up != ref_up(r)) { tgt |= 1u << st.up; n1 += 1; }
+    if (st.dn != ref_dn(r)) { tgt |= 1u << ref_dn(r); n2 += 1; }
+    const uint32_t flow = ref_flow(r);
+    const uint32_t flip = st.lower ^ flow;
+    if (flip) {
+      bool apply = ref_saddle(r);
+      if (!apply) {
+        int nl, nu;
+        link_type(st.lower, valid, nl, nu);
+        apply = (nl != ref_nlc(r)) || (nu != ref_nuc(r));
+      }
+      if (apply) {
+        n3 += __popc(flip);
+        tgt |= flip & flow;
+        if (flip & ~flow) tgt |= 1u << kSelf;
+      }
+    }
+    for (uint32_t m = tgt; m; m &= m - 1) mark_vertex(marks, slot_target(i, __ffs(m) - 1, G), G);
+    const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
+    if (T.bval && slots[i] != ns)  // benign race: every writer stores the same pass number
+      stamp(T.bslot, T.sbslot, T, x / BX, y / BY, z / BZ, (uint16_t)T.round);
+    slots[i] = ns;
+    if (ref_saddle(r)) lm[i] = st.lower | ((valid & ~st.lower) << 16);
+    if (T.act_next && tgt)
+      atomicOr(&T.act_next[(size_t)row * G.W + (x >> 5)], 1u << (x & 31));
   }
   warp_add(&cnt[C_N1 + 0], n1);
   warp_add(&cnt[C_N1 + 1], n2);

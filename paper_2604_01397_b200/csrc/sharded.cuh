@@ -158,6 +158,7 @@ struct Slab {
   GridP G{};
   dim3 sgrid;
   int zc = 1;
+  bool fast = false;  // every owned lo >= 0: k_stencil_fast
   float *f = nullptr, *g = nullptr;
   uint32_t *ref = nullptr, *marks = nullptr, *ghost_lo = nullptr, *ghost_hi = nullptr;
   uint8_t *slots = nullptr, *c = nullptr;
@@ -302,6 +303,7 @@ struct ShardedRun {
       set_err("validate", "|f - g| > eps for some vertex");
       throw Error{EXACTZ_EBOUND};
     }
+    each([&](Slab &x) { x.fast = x.hcnt[C_NEG] == 0 && !(flags & 0x800u); });
     // O7 reference of f on the owned planes
     zero_counters();
     each([&](Slab &x) {
@@ -501,8 +503,12 @@ struct ShardedRun {
     const bool c3 = !(flags & EXACTZ_NO_C3);
     zero_counters();
     each([&](Slab &x) {
-      k_stencil<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm, x.G,
-                                                        x.zc, Track{}, x.cnt);
+      if (x.fast)
+        k_stencil_fast<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
+                                                               x.G, x.zc, Track{}, x.cnt);
+      else
+        k_stencil<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm, x.G,
+                                                          x.zc, Track{}, x.cnt);
     });
     CK(cudaGetLastError());
     if (!(flags & EXACTZ_NO_C2) && nS > 1) {

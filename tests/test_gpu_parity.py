@@ -50,6 +50,8 @@ CASES = [
     ("C3", (17, 21, 150)),     # combustion recipe: many saddles, plateaus at 300 K
     ("C4", (1, 90, 300)),      # 2D climate recipe (nz = 1), 3 x-blocks
     ("C5", (24, 18, 40)),      # cosmology recipe at rel 1e-4
+    ("C2", (30, 20, 70)),      # 3 stencil tiles in x (32 wide), 3 in y (8 high)
+    ("C3", (24, 19, 66)),      # plateau ties across tile borders
 ]
 
 
@@ -57,6 +59,31 @@ CASES = [
 def test_parity_configs(exactz, oracle, cfg, shape):
     f, g, xi = S.make(cfg, shape=shape)
     assert_parity(*run_both(exactz, oracle, f, g, xi))
+
+
+def test_parity_negative_values(exactz, oracle):
+    """Fields with negative values (some lo = RU(f - xi) < 0) run the general
+    stencil instead of k_stencil_fast; parity with the oracle either way."""
+    f, _, xi = S.make("C2", shape=(30, 20, 40))
+    f2 = f - float(f.mean())
+    g2 = S.decompress(f2, xi, seed=11)
+    assert bool((f2 < 0).any())
+    assert_parity(*run_both(exactz, oracle, f2, g2, xi))
+
+
+# debug flag 0x800 of exactz_correct: the general stencil (k_stencil) even for
+# non-negative fields
+@pytest.mark.parametrize("cfg,shape,mode", [("C2", (60, 40, 100), "uniform"),
+                                            ("C3", (50, 33, 70), "uniform"),
+                                            ("C1", (40, 40, 40), "sz"),
+                                            ("C4", (1, 200, 300), "uniform")])
+def test_fast_stencil_equals_general(exactz, cfg, shape, mode):
+    f, g, xi = S.make(cfg, shape=shape, device="cuda", mode=mode)
+    a = exactz.exactz_correct(f, g, xi, stats_cap=100000)
+    b = exactz.exactz_correct(f, g, xi, flags=0x800, stats_cap=100000)
+    assert a.iters == b.iters and a.status == b.status
+    assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
+    assert a.stats == b.stats
 
 
 @pytest.mark.parametrize("cfg,shape", [("C1", None), ("C3", (12, 16, 140))])
