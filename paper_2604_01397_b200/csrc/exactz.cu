@@ -341,7 +341,7 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
   uint64_t *cpkeys = reform ? C.arena.get<uint64_t>(V) : nullptr;
   C.zero();
   C.run(EXACTZ_K_REFERENCE, 8 * (uint64_t)V, true, [&] {
-    k_reference<<<C.rgrid, C.vblock, 0, C.s>>>(f, C.G, R.ref, keys, cpkeys, C.cnt);
+    k_reference_tile<<<C.sgrid, 256, 0, C.s>>>(f, C.G, C.zc, R.ref, keys, cpkeys, C.cnt);
   });
   C.read();
   R.nS = (int)C.hcnt[C_NSADDLE];
@@ -644,8 +644,8 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   Tracking trk;
   trk.geometry(C);
   static const unsigned long long act_div = [] {
-    const char *e = std::getenv("EXACTZ_ACT_DIV");  // tuning knob (default 64)
-    return e ? std::strtoull(e, nullptr, 10) : 64ull;
+    const char *e = std::getenv("EXACTZ_ACT_DIV");  // tuning knob (default 8)
+    return e ? std::strtoull(e, nullptr, 10) : 8ull;
   }();
   static const unsigned long long cache_div = [] {
     const char *e = std::getenv("EXACTZ_CACHE_DIV");  // tuning knob (default 4)

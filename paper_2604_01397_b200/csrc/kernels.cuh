@@ -342,6 +342,87 @@ __global__ void __launch_bounds__(128) k_reference(const float *__restrict__ f, 
                        row / G.ny);
 }
 
+// The same reference on the stencil's z-marching shared-memory tile (32 x 8
+// columns per CTA, f planes z-1 .. z+1 in a 4-deep ring with halo; NaN for
+// missing neighbours): neighbour values come from shared memory instead of 14
+// global loads per vertex.
+__global__ void __launch_bounds__(256) k_reference_tile(const float *__restrict__ f, GridP G,
+                                                        int zc, uint32_t *__restrict__ ref,
+                                                        uint64_t *saddle_keys, uint64_t *cp_keys,
+                                                        unsigned long long *cnt) {
+  constexpr int TXr = 32, TYr = 8, SXr = TXr + 2, SPr = SXr * (TYr + 2);
+  __shared__ float sg[4][SPr];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, tid = threadIdx.x;
+  const int x0 = blockIdx.x * TXr, y0 = blockIdx.y * TYr;
+  const int z0 = G.zb + blockIdx.z * zc, z1 = min(z0 + zc, G.ze);
+  const int x = x0 + tx, y = y0 + ty;
+  const bool inside = x < G.nx && y < G.ny;
+  const int c = (ty + 1) * SXr + tx + 1;
+  int coff[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int cc = tid + k * 256;
+    coff[k] = -1;
+    if (cc < SPr) {
+      const int ly = cc / SXr, lx = cc - ly * SXr;
+      const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+      if (gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny) coff[k] = gx + G.nx * gy;
+    }
+  }
+  auto stage = [&](int p) {
+    const bool pin = p >= 0 && p < G.nz;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (tid + k * 256 < SPr)
+        sg[p & 3][tid + k * 256] =
+            (pin && coff[k] >= 0) ? f[(size_t)p * G.nx * G.ny + coff[k]] : __int_as_float(0x7fc00000);
+  };
+  stage(z0 - 1);
+  stage(z0);
+  for (int z = z0; z < z1; ++z) {
+    stage(z + 1);
+    __syncthreads();
+    bool isext = false, sad = false;
+    uint64_t key = 0;
+    if (inside) {
+      const float *pm = &sg[(z - 1) & 3][c], *p0 = &sg[z & 3][c], *pp = &sg[(z + 1) & 3][c];
+      float v[kSlots];
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {
+        const int b = slot_bits(s), sg1 = slot_sign(s);
+        const float *pl = (b >> 2) ? (sg1 > 0 ? pp : pm) : p0;
+        v[s] = pl[sg1 * ((b & 1) + ((b >> 1) & 1) * SXr)];
+      }
+      const Star st = eval_values(v, *p0);
+      const uint32_t valid = valid_mask(x, y, z, G);
+      int nlc, nuc;
+      link_type(st.lower, valid, nlc, nuc);
+      isext = (nlc == 0) || (nuc == 0);
+      sad = !isext && (nlc >= 2 || nuc >= 2);
+      const bool join = sad && nlc >= 2, split = sad && nuc >= 2;
+      const int i = x + G.nx * (y + G.ny * z);
+      ref[i] = st.lower | ((uint32_t)st.dn << 14) | ((uint32_t)st.up << 18) |
+               ((uint32_t)nlc << 22) | ((uint32_t)nuc << 25) | ((uint32_t)sad << 28) |
+               ((uint32_t)join << 29) | ((uint32_t)split << 30);
+      const uint32_t ig = (uint32_t)(i + G.zoff * G.nx * G.ny);
+      key = ((uint64_t)ordered_key(*p0) << 32) | ig;
+    }
+    const unsigned ms = __ballot_sync(0xffffffffu, sad);
+    const unsigned mc = cp_keys ? __ballot_sync(0xffffffffu, sad || isext) : 0u;
+    unsigned long long bs = 0, bc = 0;
+    if (tx == 0) {
+      if (ms) bs = atomicAdd(&cnt[C_NSADDLE], (unsigned long long)__popc(ms));
+      if (mc) bc = atomicAdd(&cnt[C_NCP], (unsigned long long)__popc(mc));
+    }
+    bs = __shfl_sync(0xffffffffu, bs, 0);
+    bc = __shfl_sync(0xffffffffu, bc, 0);
+    const unsigned below = (1u << tx) - 1u;
+    if (sad) saddle_keys[bs + __popc(ms & below)] = key;
+    if (cp_keys && (sad || isext)) cp_keys[bc + __popc(mc & below)] = key;
+    // (4-slot ring: the slot staged at step z+1 was last read at step z-2)
+  }
+}
+
 __global__ void k_keys_to_ids(const uint64_t *__restrict__ keys, int32_t *ids, int n) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) ids[k] = (int32_t)(keys[k] & 0xffffffffu);
