@@ -412,6 +412,9 @@ struct Tracking {
   int cur = 0;
   int32_t *list = nullptr;  // active vertices of a sparse pass (k_act_list)
   int *nlist = nullptr;
+  uint32_t *edited = nullptr;  // vertices edited by the last pass (k_count_edit)
+  bool pull_stars = true;      // this pass: edited bitmap (pulled next pass) or pushed stars
+  bool edited_valid = false;   // `edited` holds the previous pass's edits
   // C3 cache with brick stamps
   bool cache_on = false;
   int nbx = 0, nby = 0, nbz = 0, nb = 0, nsx = 0, nsy = 0, nsz = 0, nsb = 0;
@@ -435,6 +438,7 @@ struct Tracking {
     }
     list = C.arena.get<int32_t>((size_t)C.V);
     nlist = C.arena.get<int>(1);
+    edited = C.arena.get<uint32_t>(C.mark_words());
     act_on = true;
   }
   void start_cache(Ctx &C, const Reference &R) {
@@ -473,7 +477,10 @@ struct Tracking {
       T.sbval = sbval;
       T.sbslot = sbslot;
     }
-    if (act_on) T.act_next = act[cur ^ 1];
+    if (act_on) {
+      T.act_next = act[cur ^ 1];
+      T.edited = pull_stars ? edited : nullptr;
+    }
     return T;
   }
 };
@@ -507,6 +514,11 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
   // algorithmic bytes per vertex: g 4 + ref 4 read, slots 1 + mark bits 1/8
   // written; a sparse or compacted pass: the active vertices
   // only (plus the activity bitmap)
+  if (compact && trk->edited_valid) {  // this pass's set: fired | stars of last pass's edits
+    C.run(EXACTZ_K_SPARSE, (uint64_t)C.V / 4, true, [&] {
+      k_dilate_or<<<148 * 16, 256, 0, C.s>>>(trk->act[trk->cur], trk->edited, C.G);
+    });
+  }
   if (compact) {
     C.run(EXACTZ_K_SPARSE, (uint64_t)C.V / 8, true, [&] {
       k_stencil_compact<<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, trk->act[trk->cur],
@@ -533,7 +545,9 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
   } else {
     CK(cudaMemsetAsync(trk->nlist, 0, sizeof(int), C.s));
     C.run(EXACTZ_K_SPARSE, (uint64_t)C.V / 8, true, [&] {
-      k_act_list<<<148 * 16, 256, 0, C.s>>>(trk->act[trk->cur], C.G, trk->list, trk->nlist);
+      k_act_list<<<148 * 16, 256, 0, C.s>>>(trk->act[trk->cur],
+                                            trk->edited_valid ? trk->edited : nullptr, C.G,
+                                            trk->list, trk->nlist);
     });
     C.run(EXACTZ_K_SPARSE, 0, true, [&] {
       k_stencil_list<<<148 * 16, 256, 0, C.s>>>(g, R.ref, marks, slots, lm, trk->list,
@@ -563,6 +577,8 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
                                 cache ? trk->ntodo : nullptr);
   }
   C.join();
+  if (trk && trk->act_on && trk->pull_stars)  // read by this pass's stencil, rewritten below
+    CK(cudaMemsetAsync(trk->edited, 0, C.mark_words() * 4, C.s));
   // bytes: mark words read (the per-edit 14 B are added once V_t is known)
   C.run(EXACTZ_K_EDIT, (uint64_t)C.V / 8, true, [&] {
     if (trk)
@@ -573,9 +589,10 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
                                                     do_edit ? 1 : 0, T, C.cnt);
   });
   C.read();
-  if (trk && trk->act_on) {  // act_next is complete: it is the next pass's set
+  if (trk && trk->act_on) {  // act_next (| stars of `edited`) is the next pass's set
     trk->cur ^= 1;
     trk->ready = true;
+    trk->edited_valid = trk->pull_stars;
   }
   PassOut o;
   o.vt = C.hcnt[C_VT];
@@ -668,6 +685,9 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       // of the list-based ones)
       const bool force_compact = (flags & 0x400u) != 0;
       trk.sparse = !force_compact;
+      // stars of this pass's edits: pulled (dilation of an edited bitmap) when
+      // many are expected, pushed by the edit kernel when few
+      trk.pull_stars = prev_vt * 256 > (unsigned long long)V;
       if (!(flags & 0x100u) && !trk.act_on &&
           (force_compact || prev_vt * act_div <= (unsigned long long)V ||
            (compact_div && prev_vt * compact_div <= (unsigned long long)V)))

@@ -101,6 +101,7 @@ struct Track {
   uint16_t *bval, *bslot;       // brick stamps (nullptr: C3 cache off)
   uint16_t *sbval, *sbslot;     // superbrick stamps (max over its bricks)
   uint32_t *act_next;           // vertex activity for the next pass (nullptr: off)
+  uint32_t *edited;             // vertices edited by this pass (written by k_count_edit)
   int nbx, nby, nbz, round;
   int nsx, nsy;                 // superbrick grid (x, y extents)
 };
@@ -903,12 +904,48 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
   warp_add(&cnt[C_N1 + 2], n3);
 }
 
+// act |= closed stars of the vertices edited by the previous pass: the
+// edited bitmap dilated by the Freudenthal star (offsets in rows (dz, dy) of
+// the KR list; dx in {-1, 0} for rows 0..3 and {0, +1} for rows 3..6).  One
+// thread per word; the star is symmetric, so "some edited vertex lies in my
+// star" is this pull.
+__device__ __forceinline__ uint32_t dilated_word(const uint32_t *__restrict__ edited, int row,
+                                                 int wx, const GridP &G) {
+  const int z = div_ny(row, G), y = row - z * G.ny;
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const int yy = y + kr_dy(k), zz = z + kr_dz(k);
+    if (yy < 0 || yy >= G.ny || zz < 0 || zz >= G.nz) continue;
+    const uint32_t *r = edited + (size_t)(yy + G.ny * zz) * G.W;
+    const uint32_t e = __ldg(&r[wx]);
+    acc |= e;
+    if (k <= 3) acc |= (e << 1) | ((wx > 0) ? (__ldg(&r[wx - 1]) >> 31) : 0u);
+    if (k >= 3) acc |= (e >> 1) | ((wx + 1 < G.W) ? (__ldg(&r[wx + 1]) << 31) : 0u);
+  }
+  const int rem = G.nx - wx * 32;
+  if (rem < 32) acc &= (1u << rem) - 1u;
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k_dilate_or(uint32_t *__restrict__ act,
+                                                   const uint32_t *__restrict__ edited, GridP G) {
+  const int64_t w0 = (int64_t)G.ny * G.zb * G.W, nwords = (int64_t)G.ny * G.ze * G.W;
+  for (int64_t w = w0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int row = div_W((int)w, G), wx = (int)w - row * G.W;
+    const uint32_t acc = dilated_word(edited, row, wx, G);
+    if (acc) act[w] |= acc;
+  }
+}
+
 // List-based sparse pass (tracking): k_act_list compacts the activity bitmap
 // into a list of vertex indices (words consumed and cleared), then
 // k_stencil_list evaluates one listed vertex per thread (full parallelism;
 // the neighbours come from global memory, mostly L1/L2 hits).  Same rules and
 // outputs as k_stencil_sparse.
-__global__ void __launch_bounds__(256) k_act_list(uint32_t *__restrict__ act, GridP G,
+__global__ void __launch_bounds__(256) k_act_list(uint32_t *__restrict__ act,
+                                                  const uint32_t *__restrict__ edited, GridP G,
                                                   int32_t *__restrict__ list, int *count) {
   __shared__ int wsum[8], bbase;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -920,13 +957,14 @@ __global__ void __launch_bounds__(256) k_act_list(uint32_t *__restrict__ act, Gr
     uint32_t a = 0;
     int row = 0, x0 = 0;
     if (w < nwords) {
+      // this pass's set: fired last pass (act, consumed) | stars of its edits
+      row = div_W((int)w, G);
+      const int wx = (int)w - row * G.W;
+      x0 = wx * 32;
       a = act[w];
-      if (a) {
-        act[w] = 0u;
-        row = div_W((int)w, G);
-        x0 = ((int)w - row * G.W) * 32;
-        if (G.nx - x0 < 32) a &= (1u << (G.nx - x0)) - 1u;
-      }
+      if (a) act[w] = 0u;
+      if (edited) a |= dilated_word(edited, row, wx, G);
+      if (G.nx - x0 < 32) a &= (1u << (G.nx - x0)) - 1u;
     }
     const int n = __popc(a);
     int incl = n;
@@ -947,9 +985,21 @@ __global__ void __launch_bounds__(256) k_act_list(uint32_t *__restrict__ act, Gr
       bbase = tot ? atomicAdd(count, tot) : 0;
     }
     __syncthreads();
+    // coalesced writes: the warp writes one non-zero word at a time, lane l
+    // storing vertex x0 + l if its bit is set
     int k = bbase + wsum[warp] + incl - n;
     const int i0 = row * G.nx + x0;
-    for (; a; a &= a - 1) list[k++] = i0 + __ffs(a) - 1;
+    const unsigned nzw = __ballot_sync(0xffffffffu, a != 0u);
+    if ((int)__reduce_max_sync(0xffffffffu, (unsigned)n) * 2 < __popc(nzw)) {
+      for (; a; a &= a - 1) list[k++] = i0 + __ffs(a) - 1;  // few bits per word
+      a = 0;
+    }
+    for (unsigned nz = __ballot_sync(0xffffffffu, a != 0u); nz; nz &= nz - 1) {
+      const int j = __ffs(nz) - 1;
+      const uint32_t aj = __shfl_sync(0xffffffffu, a, j);
+      const int kj = __shfl_sync(0xffffffffu, k, j), ij = __shfl_sync(0xffffffffu, i0, j);
+      if ((aj >> lane) & 1u) list[kj + __popc(aj & ((1u << lane) - 1u))] = ij + lane;
+    }
     __syncthreads();
   }
 }
@@ -1589,7 +1639,7 @@ __device__ __forceinline__ bool edit_vertex(float *__restrict__ g, uint8_t *__re
 }
 
 template <bool TRACK>
-__global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
+__global__ void __launch_bounds__(256, 8) k_count_edit(float *__restrict__ g,
                                                     uint8_t *__restrict__ c,
                                                     uint32_t *__restrict__ marks,
                                                     const float *__restrict__ f, GridP G,
@@ -1641,9 +1691,12 @@ __global__ void __launch_bounds__(256) k_count_edit(float *__restrict__ g,
           const int z = div_ny((int)row, G), y = (int)row - z * G.ny;
           if (T.bval && sub == 0)
             stamp(T.bval, T.sbval, T, wx, y / BY, z / BZ, (uint16_t)(T.round + 1));
-          if (T.act_next && sub < 7) {
-            // closed stars of the edited vertices: 7 (dz, dy) rows, x-1 / x+1
-            // spill into the neighbouring words
+          if (T.edited && sub == 0) T.edited[w] = E;  // one writer per word (pulled later)
+          if (!T.edited && T.act_next && sub < 7) {
+            // few edits: push the closed stars of the edited vertices into
+            // act_next directly (7 (dz, dy) rows, x-1 / x+1 spill into the
+            // neighbouring words)
+            const int z = div_ny((int)row, G), y = (int)row - z * G.ny;
             const int dz = kr_dz(sub), dy = kr_dy(sub);
             const bool neg = sub <= 3, pos = sub >= 3;  // x-1 for rows 0..3, x+1 for 3..6
             const int yy = y + dy, zz = z + dz;
