@@ -302,8 +302,10 @@ def main():
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         tr = json.load(open(traffic_path))
-        roofline["traffic"] = tr.get(f"k_{dom}", {}).get("bytes_per_launch")
+        ent = tr.get(f"k_{dom}", {})
+        roofline["traffic"] = ent.get("bytes_per_launch")
         roofline["traffic_source"] = tr.get("source")
+        roofline["ncu"] = {k: v for k, v in ent.items() if k != "bytes_per_launch"}
     except Exception:
         pass
 

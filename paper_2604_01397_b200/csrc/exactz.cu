@@ -391,9 +391,13 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
   R.m1 = C.arena.get<int32_t>(R.nJ);
   R.M1 = C.arena.get<int32_t>(R.nP);
   // m1 / M1 by walking f's steepest paths from each saddle's link
-  if (!reform) {
+  if (!reform) {  // the two lists concurrently on the side streams
+    C.fork();
+    C.on_side(0);
     launch_events<false, true>(C, f, R.J, R.nJ, nullptr, nullptr, R.ref, R.m1, nullptr);
+    C.on_side(1);
     launch_events<true, true>(C, f, R.P, R.nP, nullptr, nullptr, R.ref, R.M1, nullptr);
+    C.join();
   }
 }
 
