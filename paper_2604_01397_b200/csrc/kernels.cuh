@@ -1004,6 +1004,47 @@ __global__ void __launch_bounds__(256) k_act_list(uint32_t *__restrict__ act,
   }
 }
 
+// One vertex's pass with neighbours from global memory (the list-based and
+// the direct dense passes): R1-R3, marks by atomics, slots / lm, tracking.
+__device__ __forceinline__ void vertex_pass(int i, const float *__restrict__ g,
+                                            const uint32_t *__restrict__ ref,
+                                            uint32_t *__restrict__ marks,
+                                            uint8_t *__restrict__ slots,
+                                            uint32_t *__restrict__ lm, const GridP &G,
+                                            const Track &T, unsigned &n1, unsigned &n2,
+                                            unsigned &n3) {
+  const int row = div_nx(i, G), x = i - row * G.nx;
+  const int z = div_ny(row, G), y = row - z * G.ny;
+  const uint32_t valid = valid_mask(x, y, z, G);
+  const Star st = eval_star(g, i, valid, G);
+  const uint32_t r = __ldg(&ref[i]);
+  uint32_t tgt = 0;
+  if (st.up != ref_up(r)) { tgt |= 1u << st.up; n1 += 1; }
+  if (st.dn != ref_dn(r)) { tgt |= 1u << ref_dn(r); n2 += 1; }
+  const uint32_t flow = ref_flow(r);
+  const uint32_t flip = st.lower ^ flow;
+  if (flip) {
+    bool apply = ref_saddle(r);
+    if (!apply) {
+      int nl, nu;
+      link_type(st.lower, valid, nl, nu);
+      apply = (nl != ref_nlc(r)) || (nu != ref_nuc(r));
+    }
+    if (apply) {
+      n3 += __popc(flip);
+      tgt |= flip & flow;
+      if (flip & ~flow) tgt |= 1u << kSelf;
+    }
+  }
+  for (uint32_t m = tgt; m; m &= m - 1) mark_vertex(marks, slot_target(i, __ffs(m) - 1, G), G);
+  const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
+  if (T.bval && slots[i] != ns)  // benign race: every writer stores the same pass number
+    stamp(T.bslot, T.sbslot, T, x / BX, y / BY, z / BZ, (uint16_t)T.round);
+  slots[i] = ns;
+  if (ref_saddle(r)) lm[i] = st.lower | ((valid & ~st.lower) << 16);
+  if (T.act_next && tgt) atomicOr(&T.act_next[(size_t)row * G.W + (x >> 5)], 1u << (x & 31));
+}
+
 __global__ void __launch_bounds__(256) k_stencil_list(const float *__restrict__ g,
                                                       const uint32_t *__restrict__ ref,
                                                       uint32_t *__restrict__ marks,
@@ -1014,40 +1055,8 @@ __global__ void __launch_bounds__(256) k_stencil_list(const float *__restrict__ 
                                                       Track T, unsigned long long *cnt) {
   const int n = *count;
   unsigned n1 = 0, n2 = 0, n3 = 0;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int i = __ldg(&list[k]);
-    const int row = div_nx(i, G), x = i - row * G.nx;
-    const int z = div_ny(row, G), y = row - z * G.ny;
-    const uint32_t valid = valid_mask(x, y, z, G);
-    const Star st = eval_star(g, i, valid, G);
-    const uint32_t r = __ldg(&ref[i]);
-    uint32_t tgt = 0;
-    if (st.up != ref_up(r)) { tgt |= 1u << st.up; n1 += 1; }
-    if (st.dn != ref_dn(r)) { tgt |= 1u << ref_dn(r); n2 += 1; }
-    const uint32_t flow = ref_flow(r);
-    const uint32_t flip = st.lower ^ flow;
-    if (flip) {
-      bool apply = ref_saddle(r);
-      if (!apply) {
-        int nl, nu;
-        link_type(st.lower, valid, nl, nu);
-        apply = (nl != ref_nlc(r)) || (nu != ref_nuc(r));
-      }
-      if (apply) {
-        n3 += __popc(flip);
-        tgt |= flip & flow;
-        if (flip & ~flow) tgt |= 1u << kSelf;
-      }
-    }
-    for (uint32_t m = tgt; m; m &= m - 1) mark_vertex(marks, slot_target(i, __ffs(m) - 1, G), G);
-    const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
-    if (T.bval && slots[i] != ns)  // benign race: every writer stores the same pass number
-      stamp(T.bslot, T.sbslot, T, x / BX, y / BY, z / BZ, (uint16_t)T.round);
-    slots[i] = ns;
-    if (ref_saddle(r)) lm[i] = st.lower | ((valid & ~st.lower) << 16);
-    if (T.act_next && tgt)
-      atomicOr(&T.act_next[(size_t)row * G.W + (x >> 5)], 1u << (x & 31));
-  }
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    vertex_pass(__ldg(&list[k]), g, ref, marks, slots, lm, G, T, n1, n2, n3);
   warp_add(&cnt[C_N1 + 0], n1);
   warp_add(&cnt[C_N1 + 1], n2);
   warp_add(&cnt[C_N1 + 2], n3);
