@@ -9,7 +9,9 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
+#include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -164,14 +166,23 @@ struct Ctx {
   cudaStream_t main_s = nullptr;
   void fork() {
     if (!side[0]) {
-      for (int k = 0; k < 2; ++k) CK(cudaStreamCreateWithFlags(&side[k], cudaStreamNonBlocking));
+      // side streams at the highest priority: their short, latency-bound
+      // kernels (C2 during the stencil) get SMs as soon as stencil CTAs retire
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      static const bool noprio = std::getenv("EXACTZ_NO_PRIO") != nullptr;  // diagnostic
+      for (int k = 0; k < 2; ++k)
+        CK(cudaStreamCreateWithPriority(&side[k], cudaStreamNonBlocking, noprio ? lo : hi));
       for (int k = 0; k < 3; ++k) CK(cudaEventCreateWithFlags(&fj[k], cudaEventDisableTiming));
     }
     main_s = s;
     CK(cudaEventRecord(fj[0], s));
     for (int k = 0; k < 2; ++k) CK(cudaStreamWaitEvent(side[k], fj[0], 0));
   }
-  void on_side(int k) { s = side[k]; }
+  void on_side(int k) {
+    static const bool serial = std::getenv("EXACTZ_SERIAL") != nullptr;  // diagnostic
+    s = serial ? main_s : side[k];
+  }
   void join() {
     for (int k = 0; k < 2; ++k) {
       CK(cudaEventRecord(fj[1 + k], side[k]));
@@ -287,6 +298,8 @@ struct Reference {
   int nS = 0, nJ = 0, nP = 0;
   int32_t *CP = nullptr;  // reformulation: all critical points sorted by (f, idx)
   int nC = 0;
+  int32_t *posS = nullptr;  // [V]: position in S of each f-saddle (other entries unused)
+  uint32_t *gS = nullptr;   // [nS]: g at S[k] (value bits), written by the stencils
 };
 
 // Sort 64-bit SoS keys (ordered(f) << 32 | idx) and keep the indices.
@@ -380,6 +393,12 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
       CK(cub::DeviceRadixSort::SortKeys(tmp, tb1, R.S, Sx, R.nS, 0, 32, C.s));
       CK(cub::DeviceSelect::If(tmp, tb2, Sx, R.J, nsel, R.nS, IsJoin{R.ref}, C.s));
       CK(cub::DeviceSelect::If(tmp, tb3, Sx, R.P, nsel + 1, R.nS, IsSplit{R.ref}, C.s));
+    });
+    // C2 by saddle values in S order: posS for the stencils' writes of gS
+    R.posS = C.arena.get<int32_t>((size_t)V);
+    R.gS = C.arena.get<uint32_t>(R.nS);
+    C.run(EXACTZ_K_REFERENCE, 8ull * R.nS, true, [&] {
+      k_scatter_pos<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(R.S, R.nS, R.posS);
     });
     int h[2];
     CK(cudaMemcpyAsync(h, nsel, sizeof(h), cudaMemcpyDeviceToHost, C.s));
@@ -501,20 +520,11 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
                                int round = 0) {
   bool c3 = !(flags & EXACTZ_NO_C3);
   C.zero();
-  const Track T = trk ? trk->track(round) : Track{};
+  Track T = trk ? trk->track(round) : Track{};
+  T.posS = R.posS;  // the stencils write g at the saddles into gS (C2 below)
+  T.gS = R.gS;
   const bool sparse = trk && trk->ready && trk->sparse;
   const bool compact = trk && trk->ready && !trk->sparse;
-  // R4 (C2) needs only the snapshot g: it runs on side stream 1 concurrently
-  // with the stencil
-  C.fork();
-  C.on_side(1);
-  if (!(flags & EXACTZ_NO_C2) && R.nS > 1) {
-    C.run(EXACTZ_K_SADDLE_ORDER, 8ull * R.nS, true, [&] {
-      k_saddle_order<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(g, R.S, R.nS, marks, C.G,
-                                                                      C.cnt);
-    });
-  }
-  C.s = C.main_s;
   // algorithmic bytes per vertex: g 4 + ref 4 read, slots 1 + mark bits 1/8
   // written; a sparse or compacted pass: the active vertices
   // only (plus the activity bitmap)
@@ -558,11 +568,17 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
                                                 trk->nlist, C.G, T, C.cnt);
     });
   }
-  // R4 (launched before the stencil on side stream 1) and the two C3 event
-  // kernels are independent (all read the snapshot g and the stencil's slots,
-  // all only OR marks and add counters): the events run on the two side
-  // streams, joined before the count/edit.
+  // R4 (C2) from the saddle values the stencil wrote in S order (gS), and
+  // the two C3 event kernels: independent (all read the snapshot and the
+  // stencil's outputs, all only OR marks and add counters); the events run
+  // on the two side streams, joined before the count/edit.
   C.fork();
+  if (!(flags & EXACTZ_NO_C2) && R.nS > 1) {
+    C.run(EXACTZ_K_SADDLE_ORDER, 8ull * R.nS, true, [&] {
+      k_saddle_order_vals<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(R.gS, R.S, R.nS,
+                                                                           marks, C.G, C.cnt);
+    });
+  }
   C.on_side(1);
   if (c3 && (flags & EXACTZ_REFORMULATED) && R.nC > 1) {
     // R7: adjacent critical points in the f order
@@ -701,8 +717,27 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
         trk.start_cache(C, R);
     }
     const bool tracked = allow_track && round < 65000 && (trk.act_on || trk.cache_on);
+    static const bool tl = std::getenv("EXACTZ_TIMELINE") != nullptr;  // diagnostic
+    cudaEvent_t ta = nullptr, tb = nullptr;
+    auto h0 = std::chrono::steady_clock::now();
+    if (tl) {
+      CK(cudaEventCreate(&ta));
+      CK(cudaEventCreate(&tb));
+      CK(cudaEventRecord(ta, s));
+    }
     PassOut o = detect_and_edit(C, R, f, out, c, marks, slots, lm, eps, delta, N, flags, may_edit,
                                 tracked ? &trk : nullptr, round);
+    if (tl) {  // GPU span of the pass (main stream) vs host wall-clock span
+      CK(cudaEventRecord(tb, s));
+      CK(cudaEventSynchronize(tb));
+      float gms = 0;
+      CK(cudaEventElapsedTime(&gms, ta, tb));
+      const double hms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+      std::fprintf(stderr, "pass %3d vt %12llu gpu %8.3f ms host %8.3f ms\n", round, o.vt, gms, hms);
+      cudaEventDestroy(ta);
+      cudaEventDestroy(tb);
+    }
     prev_vt = o.vt;
     if (stats && stats->rows && rows < stats->cap) {
       exactz_iter_stats &r = stats->rows[rows];

@@ -102,9 +102,19 @@ struct Track {
   uint16_t *sbval, *sbslot;     // superbrick stamps (max over its bricks)
   uint32_t *act_next;           // vertex activity for the next pass (nullptr: off)
   uint32_t *edited;             // vertices edited by this pass (written by k_count_edit)
+  const int32_t *posS;          // position in S of each f-saddle (single GPU; else nullptr)
+  uint32_t *gS;                 // g at S[k] (value bits), written by the stencils for C2
   int nbx, nby, nbz, round;
   int nsx, nsy;                 // superbrick grid (x, y extents)
 };
+
+// Outputs of a stencil at an f-saddle i: its g-lower / g-upper link masks
+// (for the C3 walks) and its value at its position in S (for C2).
+__device__ __forceinline__ void saddle_out(uint32_t *__restrict__ lm, const Track &T, int i,
+                                           uint32_t lower, uint32_t valid, uint32_t vbits) {
+  lm[i] = lower | ((valid & ~lower) << 16);
+  if (T.gS) T.gS[__ldg(&T.posS[i])] = vbits;
+}
 
 __device__ __forceinline__ void stamp(uint16_t *b, uint16_t *sb, const Track &T, int bx, int by,
                                       int bz, uint16_t v) {
@@ -625,7 +635,7 @@ __global__ void __launch_bounds__(NT, 5) k_stencil(const float *__restrict__ g,
                           n2, n3, ns, lower);
       if (TRACK && T.bval) schg = (slots[i] != ns);
       slots[i] = ns;
-      if (ref_saddle(r)) lm[i] = lower | ((valid & ~lower) << 16);
+      if (ref_saddle(r)) saddle_out(lm, T, i, lower, valid, __float_as_uint(sg[z & 3][c]));
     }
     if (TRACK && T.bval) {  // slot-change stamp of this warp's brick
       const unsigned chg = __ballot_sync(0xffffffffu, schg);
@@ -766,7 +776,7 @@ __global__ void __launch_bounds__(NT, 5) k_stencil_compact(const float *__restri
                                          &sg[(z + 1) & 3][c], r, valid, n1, n2, n3, ns, lower);
       if (T.bval) schg = (slots[i] != ns);
       slots[i] = ns;
-      if (ref_saddle(r)) lm[i] = lower | ((valid & ~lower) << 16);
+      if (ref_saddle(r)) saddle_out(lm, T, i, lower, valid, __float_as_uint(sg[z & 3][c]));
       if (tgt) {
         atomicOr(&fm[z & 1][ly], 1u << lx);
         for (uint32_t m = tgt; m; m &= m - 1) {
@@ -887,7 +897,7 @@ __global__ void __launch_bounds__(256) k_stencil_sparse(const float *__restrict_
       const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
       schg = slots[i] != ns;
       slots[i] = ns;
-      if (ref_saddle(r)) lm[i] = st.lower | ((valid & ~st.lower) << 16);
+      if (ref_saddle(r)) saddle_out(lm, T, i, st.lower, valid, __float_as_uint(g[i]));
     }
     if (T.bval) {
       const unsigned chg = __ballot_sync(0xffffffffu, schg);
@@ -1041,7 +1051,7 @@ __device__ __forceinline__ void vertex_pass(int i, const float *__restrict__ g,
   if (T.bval && slots[i] != ns)  // benign race: every writer stores the same pass number
     stamp(T.bslot, T.sbslot, T, x / BX, y / BY, z / BZ, (uint16_t)T.round);
   slots[i] = ns;
-  if (ref_saddle(r)) lm[i] = st.lower | ((valid & ~st.lower) << 16);
+  if (ref_saddle(r)) saddle_out(lm, T, i, st.lower, valid, __float_as_uint(g[i]));
   if (T.act_next && tgt) atomicOr(&T.act_next[(size_t)row * G.W + (x >> 5)], 1u << (x & 31));
 }
 
@@ -1079,6 +1089,30 @@ __global__ void k_saddle_order(const float *__restrict__ g, const int32_t *__res
     }
   }
   warp_add(&cnt[ci], n4);
+}
+
+// R4 from the saddle values the stencils wrote in S order (gS, value bits):
+// pair (S[k], S[k+1]) violates iff S[k+1] <_g S[k]; the f-smaller S[k] is
+// marked.  Sequential reads instead of two gathers of g.
+__global__ void k_saddle_order_vals(const uint32_t *__restrict__ gS,
+                                    const int32_t *__restrict__ S, int nS, uint32_t *marks,
+                                    GridP G, unsigned long long *cnt) {
+  unsigned n4 = 0;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k + 1 < nS) {
+    const float va = __uint_as_float(gS[k]), vb = __uint_as_float(gS[k + 1]);
+    const int a = S[k], b = S[k + 1];
+    if (vb < va || (vb == va && b < a)) {
+      mark_vertex(marks, a, G);
+      n4 = 1;
+    }
+  }
+  warp_add(&cnt[C_N1 + 3], n4);
+}
+
+__global__ void k_scatter_pos(const int32_t *__restrict__ S, int n, int32_t *pos) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) pos[S[k]] = k;
 }
 
 // Terminus of the steepest path from u (O6): follow 4-bit slot pointers.
@@ -1346,29 +1380,39 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
     }
     int best = -1;
     float bv = 0.0f;
-    int w[2] = {0, 0};
-    bool run[2] = {false, false};
+    constexpr int KW = 4;  // walks in flight per thread (the walks are latency chains)
+    int w[KW];
+    bool run[KW];
+#pragma unroll
+    for (int j = 0; j < KW; ++j) {
+      w[j] = 0;
+      run[j] = false;
+    }
     for (;;) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < KW; ++j)
         if (!run[j] && todo) {
           w[j] = s + soff[__ffs(todo) - 1];
           todo &= todo - 1;
           run[j] = true;
         }
-      if (!run[0] && !run[1]) break;
-      int sv[2];
-      bool ex[2] = {false, false};
+      bool anyrun = false;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < KW; ++j) anyrun |= run[j];
+      if (!anyrun) break;
+      int sv[KW];
+      bool ex[KW];
+#pragma unroll
+      for (int j = 0; j < KW; ++j) {
         sv[j] = 0;
+        ex[j] = false;
         if (run[j]) {
           if (SLAB && (w[j] < lo || w[j] >= hi)) ex[j] = true;
           else sv[j] = next_slot<SPLIT, FROM_REF>(w[j], slots, ref);
         }
       }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < KW; ++j) {
         if (!run[j]) continue;
         if (!ex[j] && sv[j] != kSelf) {
           w[j] += soff[sv[j]];

@@ -128,18 +128,35 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
   }
   __syncthreads();
 
+  // ref words one plane ahead and, at f-saddles, the position in S (for the
+  // gS write) one plane ahead of its use: no dependent load inside a step
+  const int i00 = x + G.nx * (y + G.ny * z0);
+  uint32_t rc = 0, rn = 0;
+  int pc = 0;
+  if (inside) {
+    rc = __ldcs(&ref[i00]);
+    if (T.gS && ref_saddle(rc)) pc = __ldg(&T.posS[i00]);
+    if (z0 + 1 < z1) rn = __ldcs(&ref[i00 + A]);
+  }
   for (int z = z0; z < z1; ++z) {
     uint32_t pre[2];
     const int pz = z + 2;
     const bool prefetch = pz <= z1;
     if (prefetch) load(pz, pre);
     if (tid < 15 && z + 1 < z1) table(z + 1, stab[(z + 1) & 1]);
+    int pn = 0;
+    uint32_t rnn = 0;
+    if (inside) {
+      const int in1 = x + G.nx * (y + G.ny * (z + 1));
+      if (T.gS && z + 1 < z1 && ref_saddle(rn)) pn = __ldg(&T.posS[in1]);
+      if (z + 2 < z1) rnn = __ldcs(&ref[in1 + A]);
+    }
 
     uint32_t tgt = 0;
     bool schg = false;
     if (inside) {
       const int i = x + G.nx * (y + G.ny * z);
-      const uint32_t r = __ldcs(&ref[i]);
+      const uint32_t r = rc;
       const uint32_t valid = vxy & valid_z(z, G);
       const uint32_t *P0 = &sb[z & 3][c];
       const uint32_t *Pm = &sb[(z - 1) & 3][c];
@@ -224,7 +241,10 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
       const uint8_t ns = (uint8_t)(dn | (up << 4));
       if (TRACK && T.bval) schg = (slots[i] != ns);
       slots[i] = ns;
-      if (ref_saddle(r)) lm[i] = lower | ((valid & ~lower) << 16);
+      if (ref_saddle(r)) {
+        lm[i] = lower | ((valid & ~lower) << 16);
+        if (T.gS) T.gS[pc] = bv[7];
+      }
     }
     if (TRACK && T.bval) {
       const unsigned chg = __ballot_sync(0xffffffffu, schg);
@@ -257,6 +277,9 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
     const int pf = z - 2;
     if (ty == (z & (TY - 1)) && pf >= z0 - 1 && pf >= 0) flush_plane(marks, wr, pf, z0, z1, x0, y0, G);
     if (prefetch) store(pz, pre);
+    rc = rn;
+    pc = pn;
+    rn = rnn;
     __syncthreads();
   }
   {
