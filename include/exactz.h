@@ -137,6 +137,19 @@ exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3]
                            uint64_t *violations, exactz_iter_stats *row, uint32_t flags,
                            void *stream);
 
+/* The Theorem 1 bound at full size:
+ * the weak / strong / reduced vulnerability graphs of (f, ghat) over mesh
+ * edges oriented u -> v when v <_f u (weak: f_u - f_v <= 2 eps; strong: weak
+ * and ghat_v >= f_u - eps, both exact in double; seed: strong and u <_ghat v)
+ * and D_max, the most vertices on a path of G_R from a seed endpoint, so
+ * that iterations <= N * D_max.  f, ghat: device, layout as exactz_correct
+ * (not validated against the bound).  out (HOST) = {D_max, |V(G_V)|,
+ * |V(G_S)|, |V(G_R)|, #seed edges}; *sweeps (HOST, may be NULL) = relaxation
+ * sweeps to the fixpoint.  Scratch ~7 bytes per vertex, freed on return. */
+exactz_status exactz_vulnerability(const float *f, const float *ghat, const int64_t dims[3],
+                                   float eps_abs, int64_t out[5], uint32_t *sweeps,
+                                   void *stream);
+
 /* xi = RN_f32(rel * (max f - min f)) computed in double (amb-19). */
 exactz_status exactz_eps_from_relative(const float *f, int64_t n, double rel, float *eps_abs,
                                        void *stream);

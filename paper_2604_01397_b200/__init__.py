@@ -53,6 +53,9 @@ _lib.exactz_correct_host.restype = C.c_int
 _lib.exactz_check.argtypes = [_P, _P, _i64p, C.c_float, C.POINTER(C.c_uint64),
                               C.POINTER(IterStats), C.c_uint32, _P]
 _lib.exactz_check.restype = C.c_int
+_lib.exactz_vulnerability.argtypes = [_P, _P, _i64p, C.c_float, C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_uint32), _P]
+_lib.exactz_vulnerability.restype = C.c_int
 _lib.exactz_eps_from_relative.argtypes = [_P, C.c_int64, C.c_double, C.POINTER(C.c_float), _P]
 _lib.exactz_eps_from_relative.restype = C.c_int
 _lib.exactz_strerror.argtypes = [C.c_int]
@@ -207,6 +210,19 @@ def exactz_check(f, g, eps: float, flags: int = 0, stream=None):
     if s != OK:
         raise ExactzError(s, "exactz_check")
     return v.value, tuple(row.n)
+
+
+def exactz_vulnerability(f, ghat, eps: float, stream=None) -> dict:
+    """Theorem 1 bound: D_max and the vulnerability graph sizes,
+    keys as oracle.vulnerability, plus the relaxation sweeps."""
+    out = (C.c_int64 * 5)()
+    sw = C.c_uint32(0)
+    s = _lib.exactz_vulnerability(_ptr(f), _ptr(ghat), _dims(f), float(eps), out, C.byref(sw),
+                                  _stream(stream))
+    if s != OK:
+        raise ExactzError(s, "exactz_vulnerability")
+    return dict(D_max=int(out[0]), GV=int(out[1]), GS=int(out[2]), GR=int(out[3]),
+                seeds=int(out[4]), sweeps=int(sw.value))
 
 
 def exactz_eps_from_relative(f, rel: float, stream=None) -> float:

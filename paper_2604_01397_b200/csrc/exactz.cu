@@ -23,6 +23,7 @@
 #include "../../include/exactz.h"
 #include "kernels.cuh"
 #include "stencil_fast.cuh"
+#include "vulnerability.cuh"
 
 #ifndef EXACTZ_GIT
 #define EXACTZ_GIT "dev"
@@ -210,6 +211,11 @@ struct Ctx {
     int64_t want = 148 * 24;
     int64_t z = cols >= want ? G.nz : (G.nz * cols + want - 1) / want;
     zc = (int)(z < 8 ? 8 : (z > 64 ? 64 : z));
+    static const int zc_env = [] {  // tuning knob (dev)
+      const char *e = std::getenv("EXACTZ_ZC");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (zc_env > 0) zc = zc_env;
     if (zc > G.nz) zc = G.nz;
     sblock = dim3(TX, TY, 1);
     sgrid = dim3((unsigned)((G.nx + TX - 1) / TX), (unsigned)((G.ny + TY - 1) / TY),
@@ -902,6 +908,63 @@ exactz_status exactz_eps_from_relative(const float *f, int64_t n, double rel, fl
     };
     double mn = unkey((uint32_t)h[C_KEYMIN]), mx = unkey((uint32_t)h[C_KEYMAX]);
     *eps_abs = (float)(rel * (mx - mn));
+    return EXACTZ_OK;
+  });
+}
+
+exactz_status exactz_vulnerability(const float *f, const float *ghat, const int64_t dims[3],
+                                   float eps_abs, int64_t out[5], uint32_t *sweeps,
+                                   void *stream) {
+  return guarded([&]() -> exactz_status {
+    int64_t V = 0;
+    if (!f || !ghat || !out) return EXACTZ_EINVAL;
+    if (check_dims(dims, &V) != EXACTZ_OK) return EXACTZ_EINVAL;
+    if (!std::isfinite(eps_abs) || !(eps_abs >= 0.0f)) return EXACTZ_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    Ctx C(s);
+    C.V = V;
+    C.init(dims);
+    uint8_t *flags = C.arena.get<uint8_t>((size_t)(V + 3) & ~(size_t)3);
+    uint16_t *smask = C.arena.get<uint16_t>(V);
+    int32_t *dep = C.arena.get<int32_t>(V);
+    CK(cudaMemsetAsync(flags, 0, (size_t)(V + 3) & ~(size_t)3, s));
+    C.zero();
+    const unsigned nb = (unsigned)blocks_for(V, 256);
+    k_vuln_classify<<<nb, 256, 0, s>>>(f, ghat, C.G, eps_abs, flags, smask, C.cnt);
+    k_vuln_init_dep<<<nb, 256, 0, s>>>(flags, (int)V, dep);
+    g_launches += 2;
+    CK(cudaGetLastError());
+    C.read();
+    const unsigned long long nseeds = C.hcnt[C_NSADDLE];
+    uint32_t n = 0;
+    for (;;) {  // sweeps to the fixpoint, checked every 4
+      CK(cudaMemsetAsync(&C.cnt[C_CHANGED], 0, sizeof(unsigned long long), s));
+      for (int k = 0; k < 4; ++k, ++n) {
+        k_vuln_relax<<<nb, 256, 0, s>>>(smask, C.G, dep, C.cnt);
+        g_launches++;
+      }
+      CK(cudaGetLastError());
+      unsigned long long ch = 0;
+      CK(cudaMemcpyAsync(&ch, &C.cnt[C_CHANGED], sizeof(ch), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (!ch) break;
+      if (n > (uint32_t)V + 8) {
+        set_err("exactz_vulnerability", "relaxation did not converge");
+        throw Error{EXACTZ_ECUDA};
+      }
+    }
+    C.zero();
+    k_vuln_gr<<<nb, 256, 0, s>>>(smask, C.G, dep, flags);
+    k_vuln_count<<<nb, 256, 0, s>>>(flags, dep, (int)V, C.cnt);
+    g_launches += 2;
+    CK(cudaGetLastError());
+    C.read();
+    out[0] = (int64_t)C.hcnt[C_KEYMAX];
+    out[1] = (int64_t)C.hcnt[C_N1 + 0];
+    out[2] = (int64_t)C.hcnt[C_N1 + 1];
+    out[3] = (int64_t)C.hcnt[C_N1 + 2];
+    out[4] = (int64_t)nseeds;
+    if (sweeps) *sweeps = n;
     return EXACTZ_OK;
   });
 }
