@@ -365,6 +365,18 @@ def main():
                   "ms_per_step": float(tr.item()), "iterations": rr.iters,
                   "speedup_vs_original": ms_step / float(tr.item())}
 
+    # ---------------- Theorem 1 at full size (NEXT-3; untimed): iterations <= N * D_max
+    thm = None
+    if not sharded:
+        t0 = time.perf_counter()
+        vb = E.exactz_vulnerability(f_run, g_run, xi)
+        torch.cuda.synchronize()
+        thm = {"D_max": vb["D_max"], "bound": 5 * vb["D_max"], "iterations": iters,
+               "holds": iters <= 5 * vb["D_max"], "G_V_pct": 100.0 * vb["GV"] / V,
+               "G_S_pct": 100.0 * vb["GS"] / V, "G_R_pct": 100.0 * vb["GR"] / V,
+               "seed_edges": vb["seeds"], "sweeps": vb["sweeps"],
+               "ms": 1e3 * (time.perf_counter() - t0)}
+
     # ---------------- CPU baseline: the oracle on a bounded crop (rank 0, N = 1)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -400,6 +412,7 @@ def main():
                     "ms_per_step": e2e_ms, "bit_equal_to_device_run": same},
             "gpu_launches": launches,
             "reformulated": reform,
+            "theorem1": thm,
             "clocks": ck,
             "version": E.version(),
         }
