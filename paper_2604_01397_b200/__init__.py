@@ -213,8 +213,8 @@ def exactz_check(f, g, eps: float, flags: int = 0, stream=None):
 
 
 def exactz_vulnerability(f, ghat, eps: float, stream=None) -> dict:
-    """Theorem 1 bound: D_max and the vulnerability graph sizes,
-    keys as oracle.vulnerability, plus the relaxation sweeps."""
+    """Theorem 1 bound: D_max, the sizes of the vulnerability
+    graphs G_V, G_S, G_R, the number of seed edges and the relaxation sweeps."""
     out = (C.c_int64 * 5)()
     sw = C.c_uint32(0)
     s = _lib.exactz_vulnerability(_ptr(f), _ptr(ghat), _dims(f), float(eps), out, C.byref(sw),

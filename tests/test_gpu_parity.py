@@ -86,6 +86,18 @@ def test_fast_stencil_equals_general(exactz, cfg, shape, mode):
     assert a.stats == b.stats
 
 
+def test_parity_stuck_fixpoint(exactz, oracle):
+    """lo-collapse (amb-17): f_0 > f_1 but RU(f_i - xi) is the same float for
+    both, so at lo the pair stays in index order and no edit can fix it:
+    ESTUCK after the pass that applied nothing, with the oracle's rows."""
+    lo = np.float32(-0.99999994)
+    f = torch.tensor([2e-8, 1e-8, 3.0])
+    g = torch.tensor([lo, lo, 3.0])
+    ro, rg, c, lmin, lmax = run_both(exactz, oracle, f, g, 1.0)
+    assert ro.status == 4 and ro.iters == 0
+    assert_parity(ro, rg, c, lmin, lmax)
+
+
 @pytest.mark.parametrize("cfg,shape", [("C1", None), ("C3", (12, 16, 140))])
 def test_parity_sz_plateaus(exactz, oracle, cfg, shape):
     """SZ-like binned decompression: plateaus everywhere, so SoS ties decide."""
