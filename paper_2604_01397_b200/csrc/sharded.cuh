@@ -174,6 +174,12 @@ struct Slab {
   int32_t *remote = nullptr, *allremote = nullptr;
   unsigned long long *cnt = nullptr, *hcnt = nullptr;  // device counters / host mirror
   unsigned long long *nrem = nullptr;                    // per-rank remote counts (p)
+  // vertex activity (list-based passes, as exactz_correct): act[cur] = this
+  // pass's set (owned planes), edited = the last pass's edits with the
+  // neighbours' boundary planes in the ghost planes
+  uint32_t *act[2] = {nullptr, nullptr}, *edited = nullptr;
+  int32_t *list = nullptr;
+  int *nlist = nullptr;
   size_t plane() const { return (size_t)G.nx * G.ny; }
   size_t words_per_plane() const { return (size_t)G.ny * G.W; }
 };
@@ -189,6 +195,8 @@ struct ShardedRun {
   int N;
   float xi, delta;
   uint32_t flags;
+  bool act_on = false, ready = false;  // vertex activity started / act[cur] valid
+  int cur = 0;
 
   ShardedRun(Transport &t, cudaStream_t st, Arena &a, std::vector<Slab> &slabs, int nx_, int ny_,
              int nz_, float xi_, int N_, uint32_t flags_)
@@ -211,6 +219,35 @@ struct ShardedRun {
   }
   void zero_counters() {
     each([&](Slab &x) { CK(cudaMemsetAsync(x.cnt, 0, C_NCOUNTERS * 8, s)); });
+  }
+
+  void start_act() {
+    each([&](Slab &x) {
+      const size_t n = (size_t)x.G.nz * x.words_per_plane();
+      for (int k = 0; k < 2; ++k) {
+        x.act[k] = A.get<uint32_t>(n);
+        CK(cudaMemsetAsync(x.act[k], 0, n * 4, s));
+      }
+      x.edited = A.get<uint32_t>(n);
+      CK(cudaMemsetAsync(x.edited, 0, n * 4, s));
+      x.list = A.get<int32_t>((size_t)x.G.V);
+      x.nlist = A.get<int>(1);
+    });
+    act_on = true;
+  }
+  // the neighbours' edits of their boundary planes into the ghost planes of
+  // `edited` (stars that cross the slab border)
+  void halo_edited() {
+    std::vector<const void *> lo, hi;
+    std::vector<void *> rlo, rhi;
+    each([&](Slab &x) {
+      const size_t W = x.words_per_plane();
+      lo.push_back(x.edited + W * 1);
+      hi.push_back(x.edited + W * x.nzl);
+      rlo.push_back(x.edited);
+      rhi.push_back(x.edited + W * (x.nzl + 1));
+    });
+    T.halo(lo, hi, rlo, rhi, sl[0].words_per_plane() * 4);
   }
 
   void halo_planes(bool of_f) {
@@ -502,14 +539,39 @@ struct ShardedRun {
   void round(bool do_edit, unsigned long long out[8]) {
     const bool c3 = !(flags & EXACTZ_NO_C3);
     zero_counters();
-    each([&](Slab &x) {
-      if (x.fast)
-        k_stencil_fast<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
-                                                               x.G, x.zc, Track{}, x.cnt);
-      else
-        k_stencil<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm, x.G,
-                                                          x.zc, Track{}, x.cnt);
-    });
+    auto track = [&](Slab &x) {
+      Track t{};
+      if (act_on) {
+        t.act_next = x.act[cur ^ 1];
+        t.edited = x.edited;
+      }
+      return t;
+    };
+    if (act_on && ready) {  // list-based pass: fired | stars of the last pass's edits
+      halo_edited();
+      each([&](Slab &x) {
+        CK(cudaMemsetAsync(x.nlist, 0, sizeof(int), s));
+        k_act_list<<<148 * 16, 256, 0, s>>>(x.act[cur], x.edited, x.G, x.list, x.nlist);
+        k_stencil_list<<<148 * 16, 256, 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm, x.list,
+                                                 x.nlist, x.G, track(x), x.cnt);
+      });
+    } else {
+      each([&](Slab &x) {
+        const Track t = track(x);
+        if (x.fast && act_on)
+          k_stencil_fast<true><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
+                                                                 x.G, x.zc, t, x.cnt);
+        else if (x.fast)
+          k_stencil_fast<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots,
+                                                                 x.lm, x.G, x.zc, t, x.cnt);
+        else if (act_on)
+          k_stencil<true><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
+                                                           x.G, x.zc, t, x.cnt);
+        else
+          k_stencil<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
+                                                            x.G, x.zc, t, x.cnt);
+      });
+    }
     CK(cudaGetLastError());
     if (!(flags & EXACTZ_NO_C2) && nS > 1) {
       std::vector<uint32_t *> b;
@@ -600,10 +662,20 @@ struct ShardedRun {
       CK(cudaGetLastError());
     }
     each([&](Slab &x) {
-      k_count_edit<false><<<148 * 8, 256, 0, s>>>(x.g, x.c, x.marks, x.f, x.G, xi, delta, N,
-                                          do_edit ? 1 : 0, Track{}, x.cnt);
+      if (act_on) {
+        CK(cudaMemsetAsync(x.edited, 0, (size_t)x.G.nz * x.words_per_plane() * 4, s));
+        k_count_edit<true><<<148 * 8, 256, 0, s>>>(x.g, x.c, x.marks, x.f, x.G, xi, delta, N,
+                                                    do_edit ? 1 : 0, track(x), x.cnt);
+      } else {
+        k_count_edit<false><<<148 * 8, 256, 0, s>>>(x.g, x.c, x.marks, x.f, x.G, xi, delta, N,
+                                                     do_edit ? 1 : 0, Track{}, x.cnt);
+      }
     });
     CK(cudaGetLastError());
+    if (act_on) {  // act_next (| stars of `edited`) is the next pass's set
+      cur ^= 1;
+      ready = true;
+    }
     allreduce_counters();
     read_counters();
     for (int k = 0; k < 8; ++k) out[k] = sl[0].hcnt[k];
@@ -652,10 +724,16 @@ static exactz_status sharded_impl(Transport &T, std::vector<const float *> f_in,
   R.setup(f_in, g_in);
   uint32_t it = 0, rows = 0;
   exactz_status st = EXACTZ_OK;
+  unsigned long long prev_vt = (unsigned long long)V;
   for (;;) {
     const bool may_edit = !(max_iters && it >= max_iters);
+    // vertex activity (list-based passes) once <= V/8 vertices are marked,
+    // from the globally reduced V_t (the same decision on every rank)
+    if (!(flags & EXACTZ_NO_TRACK) && !R.act_on && rows >= 1 && prev_vt * 8 <= (unsigned long long)V)
+      R.start_act();
     unsigned long long o[8];
     R.round(may_edit, o);
+    prev_vt = o[C_VT];
     if (stats && stats->rows && rows < stats->cap) {
       exactz_iter_stats &r = stats->rows[rows];
       r.violations = o[C_VT];
