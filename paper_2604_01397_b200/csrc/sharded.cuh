@@ -422,6 +422,13 @@ struct ShardedRun {
     }
     // m1 / M1 from f's paths, completed across slabs
     boundary_tables(true);
+    read_counters();
+    each([&](Slab &x) {
+      if (x.hcnt[C_CHANGED]) {
+        set_err("boundary_tables", "exit chains did not resolve");
+        throw Error{EXACTZ_ECUDA};
+      }
+    });
     each([&](Slab &x) {
       events<false, true>(x, x.f, x.J, x.nJ, x.m1);
       events<true, true>(x, x.f, x.P, x.nP, x.M1);
@@ -497,23 +504,20 @@ struct ShardedRun {
       });
       CK(cudaGetLastError());
       T.allgather(snd, rcv, 2 * P * sizeof(int2));
-      // every rank resolves its copy (identical inputs -> identical tables)
+      // every rank resolves its copy (identical inputs -> identical tables).
+      // A path crosses each slab border at most once per direction of travel
+      // (it descends strictly), so p rounds of exit -> entry replacement reach
+      // the fixpoint; one more round verifies it without a host round trip
+      // per round (the flag is read with the pass's counters).
       each([&](Slab &x) {
         int2 *t = up ? x.tup : x.tdn;
-        for (int round = 0;; ++round) {
-          if (round > 4 * p + 8) {
-            set_err("boundary_tables", "exit chains did not resolve");
-            throw Error{EXACTZ_ECUDA};
-          }
-          CK(cudaMemsetAsync(x.cnt + C_CHANGED, 0, 8, s));
-          const int n = (int)(2 * p * P);
+        const int n = (int)(2 * p * P);
+        for (int round = 0; round < p; ++round) {
           k_resolve<<<blocks_for(n, 256), 256, 0, s>>>(t, n, slabs_of(t), (int)P, x.cnt + C_CHANGED);
-          CK(cudaGetLastError());
-          unsigned long long ch = 0;
-          CK(cudaMemcpyAsync(&ch, x.cnt + C_CHANGED, 8, cudaMemcpyDeviceToHost, s));
-          sync();
-          if (!ch) break;
         }
+        CK(cudaMemsetAsync(x.cnt + C_CHANGED, 0, 8, s));
+        k_resolve<<<blocks_for(n, 256), 256, 0, s>>>(t, n, slabs_of(t), (int)P, x.cnt + C_CHANGED);
+        CK(cudaGetLastError());
       });
     }
   }
@@ -678,6 +682,10 @@ struct ShardedRun {
     }
     allreduce_counters();
     read_counters();
+    if (c3 && !reform && sl[0].hcnt[C_CHANGED]) {  // the boundary tables' verification round
+      set_err("boundary_tables", "exit chains did not resolve");
+      throw Error{EXACTZ_ECUDA};
+    }
     for (int k = 0; k < 8; ++k) out[k] = sl[0].hcnt[k];
     halo_planes(false);  // the edited boundary planes refresh the neighbours' ghosts
   }
