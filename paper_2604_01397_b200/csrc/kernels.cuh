@@ -15,6 +15,8 @@
 #include <stdint.h>
 
 #include "mesh.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace exz {
 
@@ -1181,6 +1183,32 @@ __global__ void k_resolve(int2 *table, int n, Slabs S, int A, unsigned long long
     ch |= (e2.x < 0);
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(changed, 1ull);
+}
+
+// All resolve rounds in one cooperative launch (grid-wide barriers between
+// rounds, the loop ends when no entry is still an exit): no host round trip
+// per round.  err is set when maxr rounds did not resolve every chain.
+__global__ void k_resolve_all(int2 *table, int n, Slabs S, int A, int maxr, unsigned *flag,
+                              unsigned long long *err) {
+  cg::grid_group grid = cg::this_grid();
+  for (int r = 0; r < maxr; ++r) {
+    // three flags: flag r % 3 is read after this round's barrier and reset
+    // two rounds later, after a barrier every reader has passed
+    unsigned *fl = flag + (r % 3);
+    if (grid.thread_rank() == 0) flag[(r + 1) % 3] = 0u;  // the next round's flag
+    unsigned ch = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      int2 e = table[i];
+      if (e.x >= 0) continue;
+      int2 e2 = table_entry(S, -e.x - 1, A);
+      table[i] = e2;
+      ch |= (e2.x < 0);
+    }
+    if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(fl, 1u);
+    grid.sync();
+    if (*(volatile unsigned *)fl == 0u) return;
+  }
+  if (grid.thread_rank() == 0) *err = 1ull;
 }
 
 // Per-saddle cache of the C3 result (tracking mode).  rnd = round it was

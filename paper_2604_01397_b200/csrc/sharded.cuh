@@ -180,6 +180,7 @@ struct Slab {
   uint32_t *act[2] = {nullptr, nullptr}, *edited = nullptr;
   int32_t *list = nullptr;
   int *nlist = nullptr;
+  unsigned *rflag = nullptr;  // k_resolve_all round flags (3)
   size_t plane() const { return (size_t)G.nx * G.ny; }
   size_t words_per_plane() const { return (size_t)G.ny * G.W; }
 };
@@ -197,6 +198,7 @@ struct ShardedRun {
   uint32_t flags;
   bool act_on = false, ready = false;  // vertex activity started / act[cur] valid
   int cur = 0;
+  int resolve_blocks = 0;  // co-resident grid of the cooperative resolve
 
   ShardedRun(Transport &t, cudaStream_t st, Arena &a, std::vector<Slab> &slabs, int nx_, int ny_,
              int nz_, float xi_, int N_, uint32_t flags_)
@@ -265,6 +267,13 @@ struct ShardedRun {
   }
 
   void setup(const std::vector<const float *> &f_in, const std::vector<const float *> &g_in) {
+    {
+      int dev = 0, nsm = 0, per = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_resolve_all, 256, 0));
+      resolve_blocks = nsm * (per > 4 ? 4 : (per < 1 ? 1 : per));
+    }
     int64_t gz0 = 0, gc = 0;
     std::vector<int> starts(p + 1);
     for (int r = 0; r < p; ++r) {
@@ -309,6 +318,7 @@ struct ShardedRun {
       x.cnt = A.get<unsigned long long>(C_NCOUNTERS);
       CK(cudaMallocHost(&x.hcnt, C_NCOUNTERS * 8));
       x.nrem = A.get<unsigned long long>(2 * p);
+      x.rflag = A.get<unsigned>(3);
       x.keys = A.get<uint64_t>(x.nzl * P);
       if (reform) x.cpkeys = A.get<uint64_t>(x.nzl * P);
       x.tdn = A.get<int2>(2 * p * P);
@@ -511,13 +521,15 @@ struct ShardedRun {
       // per round (the flag is read with the pass's counters).
       each([&](Slab &x) {
         int2 *t = up ? x.tup : x.tdn;
-        const int n = (int)(2 * p * P);
-        for (int round = 0; round < p; ++round) {
-          k_resolve<<<blocks_for(n, 256), 256, 0, s>>>(t, n, slabs_of(t), (int)P, x.cnt + C_CHANGED);
-        }
-        CK(cudaMemsetAsync(x.cnt + C_CHANGED, 0, 8, s));
-        k_resolve<<<blocks_for(n, 256), 256, 0, s>>>(t, n, slabs_of(t), (int)P, x.cnt + C_CHANGED);
-        CK(cudaGetLastError());
+        int n = (int)(2 * p * P);
+        Slabs sb = slabs_of(t);
+        int A2 = (int)P, maxr = 4 * p + 8;
+        unsigned long long *err = x.cnt + C_CHANGED;
+        CK(cudaMemsetAsync(x.rflag, 0, 3 * sizeof(unsigned), s));
+        CK(cudaMemsetAsync(err, 0, 8, s));
+        void *args[] = {&t, &n, &sb, &A2, &maxr, &x.rflag, &err};
+        CK(cudaLaunchCooperativeKernel((const void *)k_resolve_all, dim3(resolve_blocks), dim3(256),
+                                       args, 0, s));
       });
     }
   }
