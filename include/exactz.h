@@ -150,6 +150,30 @@ exactz_status exactz_vulnerability(const float *f, const float *ghat, const int6
                                    float eps_abs, int64_t out[5], uint32_t *sweeps,
                                    void *stream);
 
+/* The edit set E of a correction as a compact log (Alg. 1 "E"; P:178
+ * lossless edits; P:433 edits compressed losslessly).
+ * g_in, out, edit_counts: DEVICE, as given to / returned by exactz_correct
+ * (out = corrected field, edit_counts = opts.edit_counts).  Entries: every
+ * vertex with edit_counts > 0, in index order, as Stepped(k) when out equals
+ * k sequential steps RN(g - Delta) from g_in (Delta = RN(eps/N)), else
+ * Lossless(out value, the clamp RU(f - eps)).  Byte format "EXCE" v1
+ * (editlog.cuh): 64-byte header, then varint index gaps, a kind byte and the
+ * 4 value bytes of lossless entries; level > 0 compresses that payload with
+ * zstd at that level (libzstd.so.1 loaded at run time; EXACTZ_EUNSUPPORTED
+ * when absent).  buf (HOST) may be NULL: *bytes (HOST) then receives the
+ * size; else *bytes is the capacity on entry (EXACTZ_EINVAL and the size
+ * needed when too small) and the size written on return.  *entries (HOST,
+ * may be NULL) = number of entries. */
+exactz_status exactz_edit_log(const float *g_in, const float *out, const uint8_t *edit_counts,
+                              const int64_t dims[3], float eps_abs, uint32_t N, int level,
+                              uint8_t *buf, uint64_t *bytes, uint64_t *entries, void *stream);
+
+/* Decode an EXCE stream (buf, bytes: HOST) and apply it to g_in (DEVICE):
+ * out (DEVICE, may alias g_in) = g_in with every entry replayed (Stepped) or
+ * stored (Lossless).  EXACTZ_EINVAL on a malformed or truncated stream. */
+exactz_status exactz_edit_log_apply(const uint8_t *buf, uint64_t bytes, const float *g_in,
+                                    float *out, void *stream);
+
 /* xi = RN_f32(rel * (max f - min f)) computed in double (amb-19). */
 exactz_status exactz_eps_from_relative(const float *f, int64_t n, double rel, float *eps_abs,
                                        void *stream);

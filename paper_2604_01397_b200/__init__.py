@@ -56,6 +56,11 @@ _lib.exactz_check.restype = C.c_int
 _lib.exactz_vulnerability.argtypes = [_P, _P, _i64p, C.c_float, C.POINTER(C.c_int64),
                                       C.POINTER(C.c_uint32), _P]
 _lib.exactz_vulnerability.restype = C.c_int
+_lib.exactz_edit_log.argtypes = [_P, _P, _P, _i64p, C.c_float, C.c_uint32, C.c_int, _P,
+                                 C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _P]
+_lib.exactz_edit_log.restype = C.c_int
+_lib.exactz_edit_log_apply.argtypes = [_P, C.c_uint64, _P, _P, _P]
+_lib.exactz_edit_log_apply.restype = C.c_int
 _lib.exactz_eps_from_relative.argtypes = [_P, C.c_int64, C.c_double, C.POINTER(C.c_float), _P]
 _lib.exactz_eps_from_relative.restype = C.c_int
 _lib.exactz_strerror.argtypes = [C.c_int]
@@ -223,6 +228,36 @@ def exactz_vulnerability(f, ghat, eps: float, stream=None) -> dict:
         raise ExactzError(s, "exactz_vulnerability")
     return dict(D_max=int(out[0]), GV=int(out[1]), GS=int(out[2]), GR=int(out[3]),
                 seeds=int(out[4]), sweeps=int(sw.value))
+
+
+def exactz_edit_log(g_in, out, edit_counts, eps: float, N: int = 5, level: int = 0,
+                    stream=None):
+    """The EXCE edit log of a correction (bytes, entries); level > 0: zstd."""
+    n = C.c_uint64(0)
+    ne = C.c_uint64(0)
+    d = _dims(g_in)
+    s = _lib.exactz_edit_log(_ptr(g_in), _ptr(out), _ptr(edit_counts), d, float(eps), N, level,
+                             None, C.byref(n), C.byref(ne), _stream(stream))
+    if s != OK:
+        raise ExactzError(s, "exactz_edit_log")
+    buf = (C.c_uint8 * max(n.value, 1))()
+    s = _lib.exactz_edit_log(_ptr(g_in), _ptr(out), _ptr(edit_counts), d, float(eps), N, level,
+                             buf, C.byref(n), C.byref(ne), _stream(stream))
+    if s != OK:
+        raise ExactzError(s, "exactz_edit_log")
+    return C.string_at(buf, n.value), ne.value
+
+
+def exactz_edit_log_apply(log: bytes, g_in, out=None, stream=None):
+    """g_in with the EXCE log applied (a new device tensor unless out)."""
+    import torch
+    if out is None:
+        out = torch.empty_like(g_in)
+    b = (C.c_uint8 * len(log)).from_buffer_copy(log)
+    s = _lib.exactz_edit_log_apply(b, len(log), _ptr(g_in), _ptr(out), _stream(stream))
+    if s != OK:
+        raise ExactzError(s, "exactz_edit_log_apply")
+    return out
 
 
 def exactz_eps_from_relative(f, rel: float, stream=None) -> float:

@@ -7,9 +7,11 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 #include <algorithm>
+#include <dlfcn.h>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -24,6 +26,7 @@
 #include "kernels.cuh"
 #include "stencil_fast.cuh"
 #include "vulnerability.cuh"
+#include "editlog.cuh"
 
 #ifndef EXACTZ_GIT
 #define EXACTZ_GIT "dev"
@@ -965,6 +968,240 @@ exactz_status exactz_vulnerability(const float *f, const float *ghat, const int6
     out[3] = (int64_t)C.hcnt[C_N1 + 2];
     out[4] = (int64_t)nseeds;
     if (sweeps) *sweeps = n;
+    return EXACTZ_OK;
+  });
+}
+
+// ------------------------------------------------------------ edit log (NEXT-4)
+namespace {
+// libzstd through dlopen (the image has the runtime library, no headers)
+struct Zstd {
+  void *h = nullptr;
+  size_t (*bound)(size_t) = nullptr;
+  size_t (*comp)(void *, size_t, const void *, size_t, int) = nullptr;
+  size_t (*decomp)(void *, size_t, const void *, size_t) = nullptr;
+  unsigned (*iserr)(size_t) = nullptr;
+};
+const Zstd *zstd() {
+  static Zstd z = [] {
+    Zstd t;
+    t.h = dlopen("libzstd.so.1", RTLD_NOW | RTLD_LOCAL);
+    if (!t.h) return t;
+    t.bound = (size_t(*)(size_t))dlsym(t.h, "ZSTD_compressBound");
+    t.comp = (size_t(*)(void *, size_t, const void *, size_t, int))dlsym(t.h, "ZSTD_compress");
+    t.decomp = (size_t(*)(void *, size_t, const void *, size_t))dlsym(t.h, "ZSTD_decompress");
+    t.iserr = (unsigned (*)(size_t))dlsym(t.h, "ZSTD_isError");
+    if (!t.bound || !t.comp || !t.decomp || !t.iserr) t.h = nullptr;
+    return t;
+  }();
+  return z.h ? &z : nullptr;
+}
+struct ExceHeader {
+  char magic[4];
+  uint8_t version, codec;
+  uint16_t reserved;
+  float xi;
+  uint32_t N;
+  int64_t nx, ny, nz;
+  uint64_t entries, payload, raw;
+};
+static_assert(sizeof(ExceHeader) == 64, "EXCE header is 64 bytes");
+}  // namespace
+
+exactz_status exactz_edit_log(const float *g_in, const float *out, const uint8_t *edit_counts,
+                              const int64_t dims[3], float eps_abs, uint32_t N, int level,
+                              uint8_t *buf, uint64_t *bytes, uint64_t *entries, void *stream) {
+  return guarded([&]() -> exactz_status {
+    int64_t V = 0;
+    if (!g_in || !out || !edit_counts || !bytes) return EXACTZ_EINVAL;
+    if (check_dims(dims, &V) != EXACTZ_OK) return EXACTZ_EINVAL;
+    if (!std::isfinite(eps_abs) || !(eps_abs >= 0.0f)) return EXACTZ_EINVAL;
+    if (N == 0) N = 5;
+    if (N > 254 || level < 0) return EXACTZ_EINVAL;
+    if (level > 0 && !zstd()) {
+      set_err("exactz_edit_log", "libzstd.so.1 not available (use level 0)");
+      return EXACTZ_EUNSUPPORTED;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena A(s);
+    const float delta = eps_abs / (float)N;
+    uint8_t *kind = A.get<uint8_t>(V);
+    k_edit_kind<<<blocks_for(V, 256), 256, 0, s>>>(g_in, out, edit_counts, V, delta, (int)N, kind);
+    g_launches++;
+    CK(cudaGetLastError());
+    int64_t *idx = A.get<int64_t>(V), *nsel = A.get<int64_t>(1);
+    cub::CountingInputIterator<int64_t> it(0);
+    size_t tb = 0;
+    CK(cub::DeviceSelect::If(nullptr, tb, it, idx, nsel, V, HasEntry{kind}, s));
+    void *tmp = A.get<uint8_t>(tb);
+    CK(cub::DeviceSelect::If(tmp, tb, it, idx, nsel, V, HasEntry{kind}, s));
+    int64_t n = 0;
+    CK(cudaMemcpyAsync(&n, nsel, sizeof(n), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<uint8_t> raw;
+    if (n) {  // the raw payload is built on the GPU (lengths, scan, bytes)
+      uint8_t *ek = A.get<uint8_t>(n);
+      float *ev = A.get<float>(n);
+      uint64_t *len = A.get<uint64_t>(n + 1), *pos = A.get<uint64_t>(n + 1);
+      k_edit_gather<<<blocks_for(n, 256), 256, 0, s>>>(idx, n, kind, out, ek, ev);
+      k_edit_len<<<blocks_for(n, 256), 256, 0, s>>>(idx, ek, n, len);
+      g_launches += 2;
+      CK(cudaGetLastError());
+      CK(cudaMemsetAsync(len + n, 0, sizeof(uint64_t), s));
+      size_t ts = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, ts, len, pos, n + 1, s));
+      void *tsc = A.get<uint8_t>(ts);
+      CK(cub::DeviceScan::ExclusiveSum(tsc, ts, len, pos, n + 1, s));
+      uint64_t total_raw = 0;
+      CK(cudaMemcpyAsync(&total_raw, pos + n, 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      uint8_t *draw = A.get<uint8_t>(total_raw);
+      k_edit_write<<<blocks_for(n, 256), 256, 0, s>>>(idx, ek, ev, n, pos, draw);
+      g_launches++;
+      CK(cudaGetLastError());
+      raw.resize(total_raw);
+      CK(cudaMemcpyAsync(raw.data(), draw, total_raw, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    std::vector<uint8_t> pay;
+    uint8_t codec = 0;
+    if (level > 0 && !raw.empty()) {
+      const Zstd *z = zstd();
+      pay.resize(z->bound(raw.size()));
+      const size_t r = z->comp(pay.data(), pay.size(), raw.data(), raw.size(), level);
+      if (z->iserr(r)) {
+        set_err("exactz_edit_log", "ZSTD_compress failed");
+        return EXACTZ_ECUDA;
+      }
+      pay.resize(r);
+      codec = 1;
+    } else {
+      pay.swap(raw);
+      raw.assign(pay.begin(), pay.end());
+    }
+    ExceHeader h{};
+    std::memcpy(h.magic, "EXCE", 4);
+    h.version = 1;
+    h.codec = codec;
+    h.xi = eps_abs;
+    h.N = N;
+    h.nx = dims[0];
+    h.ny = dims[1];
+    h.nz = dims[2];
+    h.entries = (uint64_t)n;
+    h.payload = pay.size();
+    h.raw = raw.size();
+    const uint64_t total = sizeof(h) + pay.size();
+    if (entries) *entries = (uint64_t)n;
+    if (!buf) {
+      *bytes = total;
+      return EXACTZ_OK;
+    }
+    if (*bytes < total) {
+      *bytes = total;
+      set_err("exactz_edit_log", "buffer too small (*bytes = size needed)");
+      return EXACTZ_EINVAL;
+    }
+    std::memcpy(buf, &h, sizeof(h));
+    if (!pay.empty()) std::memcpy(buf + sizeof(h), pay.data(), pay.size());
+    *bytes = total;
+    return EXACTZ_OK;
+  });
+}
+
+exactz_status exactz_edit_log_apply(const uint8_t *buf, uint64_t bytes, const float *g_in,
+                                    float *out, void *stream) {
+  return guarded([&]() -> exactz_status {
+    if (!buf || !g_in || !out || bytes < sizeof(ExceHeader)) return EXACTZ_EINVAL;
+    ExceHeader h;
+    std::memcpy(&h, buf, sizeof(h));
+    int64_t V = 0;
+    const int64_t dims[3] = {h.nx, h.ny, h.nz};
+    if (std::memcmp(h.magic, "EXCE", 4) || h.version != 1 || h.codec > 1 || h.N < 1 ||
+        h.N > 254 || check_dims(dims, &V) != EXACTZ_OK || sizeof(h) + h.payload > bytes) {
+      set_err("exactz_edit_log_apply", "malformed EXCE stream");
+      return EXACTZ_EINVAL;
+    }
+    std::vector<uint8_t> raw;
+    const uint8_t *pay = buf + sizeof(h);
+    if (h.codec == 1) {
+      const Zstd *z = zstd();
+      if (!z) {
+        set_err("exactz_edit_log_apply", "libzstd.so.1 not available");
+        return EXACTZ_EUNSUPPORTED;
+      }
+      raw.resize(h.raw);
+      const size_t r = z->decomp(raw.data(), raw.size(), pay, h.payload);
+      if (z->iserr(r) || r != h.raw) {
+        set_err("exactz_edit_log_apply", "corrupt zstd payload");
+        return EXACTZ_EINVAL;
+      }
+    } else {
+      if (h.payload != h.raw) return EXACTZ_EINVAL;
+      raw.assign(pay, pay + h.payload);
+    }
+    std::vector<int64_t> hi;
+    std::vector<uint8_t> hk;
+    std::vector<float> hv;
+    hi.reserve(h.entries);
+    size_t p = 0;
+    int64_t prev = -1;
+    for (uint64_t e = 0; e < h.entries; ++e) {
+      uint64_t d = 0;
+      int sh = 0;
+      for (;;) {
+        if (p >= raw.size() || sh > 63) {
+          set_err("exactz_edit_log_apply", "truncated EXCE payload");
+          return EXACTZ_EINVAL;
+        }
+        const uint8_t b = raw[p++];
+        d |= (uint64_t)(b & 0x7F) << sh;
+        sh += 7;
+        if (!(b & 0x80)) break;
+      }
+      const int64_t i = prev + 1 + (int64_t)d;
+      if (i >= V || p >= raw.size()) {
+        set_err("exactz_edit_log_apply", "entry out of range or truncated");
+        return EXACTZ_EINVAL;
+      }
+      prev = i;
+      const uint8_t k = raw[p++];
+      float v = 0.0f;
+      if (k == 0) {
+        if (p + 4 > raw.size()) {
+          set_err("exactz_edit_log_apply", "truncated EXCE payload");
+          return EXACTZ_EINVAL;
+        }
+        std::memcpy(&v, &raw[p], 4);
+        p += 4;
+      } else if (k > h.N) {
+        set_err("exactz_edit_log_apply", "stepped count above N");
+        return EXACTZ_EINVAL;
+      }
+      hi.push_back(i);
+      hk.push_back(k);
+      hv.push_back(v);
+    }
+    if (p != raw.size()) {
+      set_err("exactz_edit_log_apply", "trailing bytes in the EXCE payload");
+      return EXACTZ_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena A(s);
+    if (out != g_in) CK(cudaMemcpyAsync(out, g_in, V * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    const int64_t n = (int64_t)hi.size();
+    if (n) {
+      int64_t *di = A.get<int64_t>(n);
+      uint8_t *dk = A.get<uint8_t>(n);
+      float *dv = A.get<float>(n);
+      CK(cudaMemcpyAsync(di, hi.data(), n * 8, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dk, hk.data(), n, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dv, hv.data(), n * 4, cudaMemcpyHostToDevice, s));
+      k_edit_apply<<<blocks_for(n, 256), 256, 0, s>>>(di, dk, dv, n, g_in, out, h.xi / (float)h.N);
+      g_launches++;
+      CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(s));
     return EXACTZ_OK;
   });
 }
