@@ -1494,7 +1494,7 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
   unsigned hit = 0;
   if (k < n) {
     const uint16_t rnd = EC.rnd[k];
-    const unsigned long long mask = EC.mask[k];
+    const unsigned long long mask = rnd ? EC.mask[k] : 0ull;  // written with rnd
     valid = rnd != 0 && !(mask & kFar);
     if (valid) {
       const int s = sl[k];
