@@ -382,19 +382,29 @@ __global__ void __launch_bounds__(256) k_reference_tile(const float *__restrict_
       if (gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny) coff[k] = gx + G.nx * gy;
     }
   }
-  auto stage = [&](int p) {
+  auto load = [&](int p, float (&r)[2]) {
     const bool pin = p >= 0 && p < G.nz;
 #pragma unroll
     for (int k = 0; k < 2; ++k)
-      if (tid + k * 256 < SPr)
-        sg[p & 3][tid + k * 256] =
-            (pin && coff[k] >= 0) ? f[(size_t)p * G.nx * G.ny + coff[k]] : __int_as_float(0x7fc00000);
+      r[k] = (pin && coff[k] >= 0) ? f[(size_t)p * G.nx * G.ny + coff[k]] : __int_as_float(0x7fc00000);
   };
-  stage(z0 - 1);
-  stage(z0);
+  auto store = [&](int p, const float (&r)[2]) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (tid + k * 256 < SPr) sg[p & 3][tid + k * 256] = r[k];
+  };
+  {
+    float r[2];
+    for (int p = z0 - 1; p <= z0 + 1; ++p) {
+      load(p, r);
+      store(p, r);
+    }
+  }
+  __syncthreads();
   for (int z = z0; z < z1; ++z) {
-    stage(z + 1);
-    __syncthreads();
+    float pre[2];  // plane z+2 in flight while plane z is classified
+    const bool prefetch = z + 2 <= z1;
+    if (prefetch) load(z + 2, pre);
     bool isext = false, sad = false;
     uint64_t key = 0;
     if (inside) {
@@ -432,7 +442,8 @@ __global__ void __launch_bounds__(256) k_reference_tile(const float *__restrict_
     const unsigned below = (1u << tx) - 1u;
     if (sad) saddle_keys[bs + __popc(ms & below)] = key;
     if (cp_keys && (sad || isext)) cp_keys[bc + __popc(mc & below)] = key;
-    // (4-slot ring: the slot staged at step z+1 was last read at step z-2)
+    if (prefetch) store(z + 2, pre);  // ring slot of plane z-2, last read at step z-1
+    __syncthreads();
   }
 }
 
