@@ -1648,7 +1648,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
     EC.tgt[k] = target;
     if (target >= 0) {
       mark_vertex(marks, target, G);
-      hit = 1;
+      ++hit;  // a lane may recompute several saddles (grid-stride)
     }
   }
   warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);

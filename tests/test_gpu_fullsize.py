@@ -77,3 +77,17 @@ def test_fullsize_c1_is_parity(exactz, oracle):
     assert rg.iters == ro.iters
     assert np.array_equal(rg.out.cpu().numpy().reshape(-1).view(np.uint32),
                           ro.out.view(np.uint32))
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C3"])
+def test_fullsize_tracking_equals_dense(exactz, cfg):
+    """At full size the C3 recompute list outgrows one lane per saddle (the
+    grid-stride path of k_events_cached): the tracked run must still give the
+    dense run's bits and every per-pass counter, and repeat bit for bit."""
+    f, g, xi = S.make(cfg, device="cuda")
+    runs = [exactz.exactz_correct(f, g, xi, stats_cap=100000) for _ in range(3)]
+    b = exactz.exactz_correct(f, g, xi, flags=exactz.NO_TRACK, stats_cap=100000)
+    for a in runs:
+        assert a.iters == b.iters and a.status == b.status
+        assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
+        assert a.stats == b.stats
