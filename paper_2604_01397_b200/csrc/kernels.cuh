@@ -1741,6 +1741,9 @@ __global__ void __launch_bounds__(256, 8) k_count_edit(float *__restrict__ g,
   const unsigned gmask = 0xffu << (lane & 24);  // the 8 lanes of a word
   const int64_t nwords = (int64_t)G.ny * G.ze * G.W;  // owned rows: [zb*ny, ze*ny)
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec4 = (G.nx & 3) == 0 && ((reinterpret_cast<uintptr_t>(f) |
+                                          reinterpret_cast<uintptr_t>(g)) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(c) & 3) == 0;
   unsigned vt = 0, ap = 0;
   for (int64_t w0 = (int64_t)G.ny * G.zb * G.W +
                     (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
@@ -1767,7 +1770,37 @@ __global__ void __launch_bounds__(256, 8) k_count_edit(float *__restrict__ g,
       const uint32_t bits = (word >> (4 * sub)) & 15u;
       const size_t base = (size_t)G.nx * row + (size_t)wx * 32 + 4 * sub;
       uint32_t e = 0;  // edited vertices of this word (bit = x - 32 wx)
-      if (do_edit) {
+      if (do_edit && bits && vec4) {
+        // rows of a multiple of 4: the lane's 4 vertices as one 16-byte f and
+        // g load and one 4-byte c load (independent, in flight together);
+        // written back whole (the unmarked ones unchanged)
+        const float4 fv = *reinterpret_cast<const float4 *>(f + base);
+        float4 gv = *reinterpret_cast<const float4 *>(g + base);
+        uint32_t cv = *reinterpret_cast<const uint32_t *>(c + base);
+        float *ga = reinterpret_cast<float *>(&gv);
+        const float fa[4] = {fv.x, fv.y, fv.z, fv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (!((bits >> q) & 1u)) continue;
+          const float lo = __fsub_ru(fa[q], xi);
+          if (ga[q] == lo) continue;
+          const int ci = (cv >> (8 * q)) & 0xFFu;
+          float t;
+          if (ci < N) {
+            t = __fsub_rn(ga[q], delta);
+            t = (t < lo) ? lo : t;
+          } else {
+            t = lo;
+          }
+          ga[q] = t;
+          cv = (cv & ~(0xFFu << (8 * q))) | ((uint32_t)((ci + 1) & 0xFF) << (8 * q));
+          e |= 1u << (4 * sub + q);
+        }
+        if (e) {
+          *reinterpret_cast<float4 *>(g + base) = gv;
+          *reinterpret_cast<uint32_t *>(c + base) = cv;
+        }
+      } else if (do_edit) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if ((bits >> q) & 1u)

@@ -129,6 +129,22 @@ def test_parity_alias_out(exactz, oracle):
     assert_parity(*run_both(exactz, oracle, f, g, xi, mode_alias=True))
 
 
+def test_misaligned_buffers(exactz):
+    """Device buffers one element off 16-byte alignment take the scalar edit
+    path of k_count_edit; the bits equal the aligned run."""
+    f, g, xi = S.make("C2", shape=(24, 20, 64), device="cuda")
+    a = exactz.exactz_correct(f, g, xi, stats_cap=1000)
+    fb = torch.empty(f.numel() + 1, device="cuda")
+    gb = torch.empty(g.numel() + 1, device="cuda")
+    fb[1:] = f.flatten()
+    gb[1:] = g.flatten()
+    ob = torch.empty(g.numel() + 1, device="cuda")
+    b = exactz.exactz_correct(fb[1:].view(f.shape), gb[1:].view(g.shape), xi,
+                              out=ob[1:].view(g.shape), stats_cap=1000)
+    assert a.iters == b.iters and a.stats == b.stats
+    assert torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
+
+
 def test_edit_strategy_1x3(exactz, oracle):
     """fig:edit_strategy as a 1x3 field (tests/golden/)."""
     f = torch.tensor([3.0, 1.0, 2.0])
