@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="exactz", choices=["exactz", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ocr", action="store_true", help="skip the SZ-like OCR report")
     ap.add_argument("--cpu-sample", type=int, default=64, help="edge of the oracle's crop")
     ap.add_argument("--no-reformulated", action="store_true",
                     help="skip the extra timing of the reformulated constraints (NEXT-1)")
@@ -398,6 +399,29 @@ def main():
                 "encode_ms_raw": 1e3 * (t1 - t0)}
         del ce, log0, log3
 
+    # ---------------- OCR against the SZ-like base stream (NEXT-4; untimed):
+    # the same field decompressed through SZ-like bins (synth/szlike.py), its
+    # base stream size, the correction of that input and its edit log
+    ocr = None
+    if not sharded and not args.no_ocr:
+        from synth import szlike as Z
+        del out
+        torch.cuda.empty_cache()
+        f_sz = f_run
+        g_sz = S.decompress(f_sz, xi, 0, mode="sz")
+        enc = Z.encode(f_sz, xi, g_sz)
+        c_sz = torch.empty(V, dtype=torch.uint8, device=dev)
+        r_sz = E.exactz_correct(f_sz, g_sz, xi, edit_counts=c_sz)
+        lg, ne_sz = E.exactz_edit_log(g_sz, r_sz.out, c_sz, xi, level=3)
+        ocr = {"input": "same f, ghat = SZ-like bins 2 xi round(f / 2 xi) (decompress mode sz)",
+               "base": "Lorenzo residuals of the bin codes, zigzag bytes + escapes, zstd -3",
+               "base_bytes": enc["bytes"], "CR": 4.0 * V / enc["bytes"],
+               "iterations": r_sz.iters, "status": r_sz.status,
+               "edit_entries": ne_sz, "edit_pct": 100.0 * ne_sz / V,
+               "edit_log_bytes_zstd3": len(lg),
+               "OCR": 4.0 * V / (enc["bytes"] + len(lg))}
+        del g_sz, c_sz, r_sz, lg, enc
+
     # ---------------- CPU baseline: the oracle on a bounded crop (rank 0, N = 1)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -435,6 +459,7 @@ def main():
             "reformulated": reform,
             "theorem1": thm,
             "edit_log": elog,
+            "ocr": ocr,
             "clocks": ck,
             "version": E.version(),
         }

@@ -39,3 +39,30 @@ def test_offset_rule():
     for cfg, shape in (("C1", None), ("C2", (16, 16, 16)), ("C3", (16, 16, 16))):
         f, g, xi = S.make(cfg, shape=shape)
         assert float(f.min()) >= xi
+
+
+def test_szlike_roundtrip():
+    """The SZ-like base stream (synth/szlike.py) decodes to the generator's
+    ghat bit for bit, 3D and 2D, with exception entries (vertices off the
+    RN_f32(2 xi q) grid, here injected one ulp away) and escapes (large
+    Lorenzo residuals, here a spike)."""
+    from synth import szlike as Z
+    for cfg, shape in [("C2", (20, 24, 37)), ("C4", (1, 30, 50)), ("C3", (9, 16, 16))]:
+        f, g, xi = S.make(cfg, shape=shape, mode="sz")
+        e = Z.encode(f, xi, g)
+        assert torch.equal(Z.decode(e).view(torch.int32), g.view(torch.int32))
+        g2 = g.clone().reshape(-1)
+        idx = torch.tensor([0, 7, 8, g2.numel() - 1])
+        g2[idx] = torch.nextafter(g2[idx], torch.full_like(g2[idx], float("inf")))
+        g2 = g2.reshape(g.shape)
+        f2 = f.clone().reshape(-1)
+        f2[5] += 3000 * 2 * xi  # a spike: residuals beyond one byte
+        f2 = f2.reshape(f.shape)
+        q = torch.round(f2.double() / (2 * float(np.float32(xi))))
+        g3 = (2 * float(np.float32(xi)) * q).float()
+        e3 = Z.encode(f2, xi, g3)
+        assert e3["n_esc"] >= 1 and e3["n_exc"] == 0
+        assert torch.equal(Z.decode(e3).view(torch.int32), g3.view(torch.int32))
+        e4 = Z.encode(f, xi, g2)
+        assert e4["n_exc"] == 4
+        assert torch.equal(Z.decode(e4).view(torch.int32), g2.view(torch.int32))
