@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *FLAGS, f"-DEXACTZ_GIT=\"{_git()}\"", "-I", os.path.join(ROOT, "include"),
-           "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES], "-lnccl"]
+           "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES], "-lnccl",
+           *os.environ.get("EXACTZ_NVCC_EXTRA", "").split()]  # dev knob (tuning builds)
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
