@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
                                                         unsigned long long *cnt) {
   __shared__ uint32_t sb[4][SP];  // staged value bits, 4-plane ring
   __shared__ __align__(16) u64 wr[4][TY][8];  // mark rows by writer (k_stencil)
-  __shared__ int stab[2][16];     // per step: star position -> word offset from the centre cell
+  __shared__ int stab[4][16];     // per z mod 4: star position -> word offset from the centre cell
   __shared__ uint8_t sslot[16];   // star position -> slot code
   const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
@@ -103,8 +103,7 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
     for (int k = 0; k < 2; ++k)
       if (tid + k * NT < SP) sb[p & 3][tid + k * NT] = r[k];
   };
-  auto table = [&](int z, int *dst) {  // thread q < 15: entry of star position q for step z
-    const int q = tid;
+  auto table = [&](int z, int q, int *dst) {  // entry of star position q for steps = z mod 4
     int dx = 0, dy = 0, dz = 0;
     if (q != 7) {
       const int s = q < 7 ? q : q - 1;
@@ -115,10 +114,8 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
     }
     dst[q] = (((z + dz) & 3) - (z & 3)) * SP + dy * SX + dx;
   };
-  if (tid < 15) {
-    sslot[tid] = (uint8_t)(tid < 7 ? tid : (tid == 7 ? kSelf : tid - 1));
-    table(z0, stab[z0 & 1]);
-  }
+  if (tid < 15) sslot[tid] = (uint8_t)(tid < 7 ? tid : (tid == 7 ? kSelf : tid - 1));
+  if (tid < 60) table(tid / 15, tid % 15, stab[tid / 15]);
   {  // prologue: planes z0-1, z0, z0+1
     uint32_t r[2];
     for (int p = z0 - 1; p <= z0 + 1; ++p) {
@@ -143,7 +140,6 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
     const int pz = z + 2;
     const bool prefetch = pz <= z1;
     if (prefetch) load(pz, pre);
-    if (tid < 15 && z + 1 < z1) table(z + 1, stab[(z + 1) & 1]);
     int pn = 0;
     uint32_t rnn = 0;
     if (inside) {
@@ -207,7 +203,7 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
                       umin3(bv[6], bv[7], bv[8])),
                 umin3(bv[9], bv[10], bv[11]), umin3(bv[12], bv[13], bv[14]));
       const int wu = qmax & 15, wd = (int)(qmin & 15u);
-      const int *tb = stab[z & 1];
+      const int *tb = stab[z & 3];
       int up = sslot[wu], dn = sslot[wd];
       if ((int)P0[tb[wu]] != emax || P0[tb[wd]] != emin) {
         // a bucket held two different values: the exact sequential scan
