@@ -270,9 +270,15 @@ __device__ __forceinline__ uint32_t ordered_key(float v) {
 }
 
 // mark bitmap: row-padded, bit x of word row*W + x/32 (row = y + ny*z)
+// Marks only accumulate until the edit pass clears them, so a bit already
+// set (by the stencil, which ran before, or by another rule) needs no atomic:
+// an L2 read (the 16 MB bitmap of 512^3 stays resident) replaces most
+// read-modify-writes in the dense rounds, where most targets are marked.
 __device__ __forceinline__ void mark_vertex(uint32_t *marks, int v, const GridP &G) {
   const int row = div_nx(v, G), x = v - row * G.nx;
-  atomicOr(&marks[(size_t)row * G.W + (x >> 5)], 1u << (x & 31));
+  uint32_t *w = &marks[(size_t)row * G.W + (x >> 5)];
+  const uint32_t b = 1u << (x & 31);
+  if (!(__ldcg(w) & b)) atomicOr(w, b);
 }
 
 __device__ __forceinline__ bool sos_less_g(const float *h, int u, int v) {
