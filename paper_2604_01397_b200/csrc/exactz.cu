@@ -486,6 +486,7 @@ struct Tracking {
       e.mask = C.arena.get<unsigned long long>(n);
       e.tgt = C.arena.get<int32_t>(n);
       CK(cudaMemsetAsync(e.rnd, 0, (size_t)(n ? n : 1) * 2, C.s));
+      CK(cudaMemsetAsync(e.mask, 0, (size_t)(n ? n : 1) * 8, C.s));  // read with rnd
       return e;
     };
     ecJ = cache(R.nJ);

@@ -995,6 +995,7 @@ __global__ void __launch_bounds__(256) k_act_list(uint32_t *__restrict__ act,
       if (edited) a |= dilated_word(edited, row, wx, G);
       if (G.nx - x0 < 32) a &= (1u << (G.nx - x0)) - 1u;
     }
+    if (!__syncthreads_or(a != 0u)) continue;  // nothing active in these 256 words
     const int n = __popc(a);
     int incl = n;
 #pragma unroll
@@ -1511,23 +1512,38 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
   unsigned hit = 0;
   if (k < n) {
     const uint16_t rnd = EC.rnd[k];
-    const unsigned long long mask = rnd ? EC.mask[k] : 0ull;  // written with rnd
+    const unsigned long long mask = EC.mask[k];  // zeroed when the cache started
     valid = rnd != 0 && !(mask & kFar);
     if (valid) {
       const int s = sl[k];
       const int yz = div_nx(s, G), sz = div_ny(yz, G), sx = s - yz * G.nx, sy = yz - sz * G.ny;
       const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
-      for (uint32_t m = (uint32_t)mask; m && valid; m &= m - 1) {
-        const int j = __ffs(m) - 1;
-        const int dz = j / 9 - 1, dy = (j / 3) % 3 - 1, dx = j % 3 - 1;
-        const int nb = (bsx + dx) + T.nbx * ((bsy + dy) + T.nby * (bsz + dz));
-        if (T.bval[nb] > rnd || T.bslot[nb] > rnd) valid = false;
-      }
-      for (uint32_t m = (uint32_t)(mask >> 32); m && valid; m &= m - 1) {
-        const int j = __ffs(m) - 1;
-        const int dz = j / 9 - 1, dy = (j / 3) % 3 - 1, dx = j % 3 - 1;
-        const int nb = (bsx / SB + dx) + T.nsx * ((bsy / SB + dy) + T.nsy * (bsz / SB + dz));
-        if (T.sbval[nb] > rnd || T.sbslot[nb] > rnd) valid = false;
+      // the stamps of up to 4 bricks in flight per step (independent loads)
+      uint32_t m = (uint32_t)mask, ms = (uint32_t)(mask >> 32);
+      while ((m | ms) && valid) {
+        uint16_t st[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          st[2 * q] = st[2 * q + 1] = 0;
+          if (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const int dz = j / 9 - 1, dy = (j / 3) % 3 - 1, dx = j % 3 - 1;
+            const int nb = (bsx + dx) + T.nbx * ((bsy + dy) + T.nby * (bsz + dz));
+            st[2 * q] = T.bval[nb];
+            st[2 * q + 1] = T.bslot[nb];
+          } else if (ms) {
+            const int j = __ffs(ms) - 1;
+            ms &= ms - 1;
+            const int dz = j / 9 - 1, dy = (j / 3) % 3 - 1, dx = j % 3 - 1;
+            const int nb = (bsx / SB + dx) + T.nsx * ((bsy / SB + dy) + T.nsy * (bsz / SB + dz));
+            st[2 * q] = T.sbval[nb];
+            st[2 * q + 1] = T.sbslot[nb];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (st[q] > rnd) valid = false;
       }
     }
     if (valid) {
