@@ -43,6 +43,8 @@ class Opts(C.Structure):
                 ("label_max", C.c_void_p), ("stats", C.POINTER(Stats))]
 
 
+import torch  # noqa: E402,F401  (first: libtorch_cuda and libexactz share torch's libnccl.so.2)
+
 _lib = C.CDLL(LIB_PATH)
 _P, _i64p = C.c_void_p, C.POINTER(C.c_int64)
 _lib.exactz_correct.argtypes = [_P, _P, _i64p, C.c_float, _P, C.POINTER(C.c_uint32),

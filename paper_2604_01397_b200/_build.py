@@ -37,7 +37,26 @@ def stale() -> bool:
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "exactz.h"))
+    deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _nccl_link() -> list:
+    """Link the NCCL that torch bundles (nvidia-nccl wheel), with an rpath to it.
+
+    Linking the system libnccl.so.2 (an older 2.27) made whichever library
+    loaded first own the soname: loading libexactz.so before `import torch`
+    left libtorch_cuda.so without the 2.28 symbols it needs."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia")
+        for base in (spec.submodule_search_locations or []):
+            d = os.path.join(base, "nccl", "lib")
+            if os.path.exists(os.path.join(d, "libnccl.so.2")):
+                return ["-L", d, "-l:libnccl.so.2", "-Xlinker", f"-rpath={d}"]
+    except Exception:
+        pass
+    return ["-lnccl"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -45,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *FLAGS, f"-DEXACTZ_GIT=\"{_git()}\"", "-I", os.path.join(ROOT, "include"),
-           "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES], "-lnccl",
+           "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES], *_nccl_link(),
            *os.environ.get("EXACTZ_NVCC_EXTRA", "").split()]  # dev knob (tuning builds)
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
