@@ -235,14 +235,14 @@ def main():
 
         def step(profile=False):
             return E.exactz_correct_sharded(comm, f_run, g_run, dims, xi, out=out,
-                                            stats_cap=100000)
+                                            stats_cap=1024)  # per-pass rows (paper: <= 612 passes)
     else:
         f_run, g_run = f, g
         out = torch.empty_like(g)
 
         def step(profile=False):
             return E.exactz_correct(f, g, xi, out=out, flags=E.PROFILE if profile else 0,
-                                    stats_cap=100000)
+                                    stats_cap=1024)  # per-pass rows (paper: <= 612 passes)
 
     for _ in range(args.warmup):
         r0 = step()
