@@ -230,7 +230,7 @@ struct Ctx {
       int64_t rows = (int64_t)G.ny * G.nz, by = (148 * 16 + bx - 1) / bx;
       rgrid = dim3(bx, (unsigned)(rows < by ? rows : by), 1);
     }
-    cnt = arena.get<unsigned long long>(C_NCOUNTERS);
+    cnt = arena.get<unsigned long long>(C_NALLOC);
     CK(cudaMallocHost(&hcnt, C_NCOUNTERS * sizeof(unsigned long long)));
     upload_lut();
   }
@@ -255,8 +255,10 @@ struct Ctx {
     CK(cudaMemcpyToSymbolAsync(d_comp, lut, sizeof(lut), 0, cudaMemcpyHostToDevice, s));
   }
   size_t mark_words() const { return (size_t)G.ny * G.nz * G.W; }
-  void zero() { CK(cudaMemsetAsync(cnt, 0, C_NCOUNTERS * sizeof(unsigned long long), s)); }
+  void zero() { CK(cudaMemsetAsync(cnt, 0, C_NALLOC * sizeof(unsigned long long), s)); }
   void read() {
+    k_fold_counters<<<1, 32, 0, s>>>(cnt);  // warp_add replicas -> cnt[0 .. C_NCOUNTERS)
+    g_launches++;
     CK(cudaMemcpyAsync(hcnt, cnt, C_NCOUNTERS * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -894,7 +896,8 @@ exactz_status exactz_eps_from_relative(const float *f, int64_t n, double rel, fl
     if (!f || n < 1 || !eps_abs || !std::isfinite(rel) || rel < 0) return EXACTZ_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     Arena A(s);
-    unsigned long long *cnt = A.get<unsigned long long>(C_NCOUNTERS);
+    unsigned long long *cnt = A.get<unsigned long long>(C_NALLOC);
+    CK(cudaMemsetAsync(cnt, 0, C_NALLOC * 8, s));
     unsigned long long init[C_NCOUNTERS] = {};
     init[C_KEYMIN] = 0xffffffffull;
     CK(cudaMemcpyAsync(cnt, init, sizeof(init), cudaMemcpyHostToDevice, s));

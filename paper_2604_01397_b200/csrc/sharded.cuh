@@ -215,12 +215,14 @@ struct ShardedRun {
   void sync() { CK(cudaStreamSynchronize(s)); }
   void read_counters() {
     each([&](Slab &x) {
+      k_fold_counters<<<1, 32, 0, s>>>(x.cnt);  // warp_add replicas (kernels.cuh)
+      g_launches++;
       CK(cudaMemcpyAsync(x.hcnt, x.cnt, C_NCOUNTERS * 8, cudaMemcpyDeviceToHost, s));
     });
     sync();
   }
   void zero_counters() {
-    each([&](Slab &x) { CK(cudaMemsetAsync(x.cnt, 0, C_NCOUNTERS * 8, s)); });
+    each([&](Slab &x) { CK(cudaMemsetAsync(x.cnt, 0, C_NALLOC * 8, s)); });
   }
 
   void start_act() {
@@ -315,7 +317,7 @@ struct ShardedRun {
       x.marks = A.get<uint32_t>((size_t)G.nz * x.words_per_plane());
       x.ghost_lo = A.get<uint32_t>(x.words_per_plane());
       x.ghost_hi = A.get<uint32_t>(x.words_per_plane());
-      x.cnt = A.get<unsigned long long>(C_NCOUNTERS);
+      x.cnt = A.get<unsigned long long>(C_NALLOC);
       CK(cudaMallocHost(&x.hcnt, C_NCOUNTERS * 8));
       x.nrem = A.get<unsigned long long>(2 * p);
       x.rflag = A.get<unsigned>(3);
@@ -547,7 +549,11 @@ struct ShardedRun {
 
   void allreduce_counters() {
     std::vector<unsigned long long *> b;
-    each([&](Slab &x) { b.push_back(x.cnt); });
+    each([&](Slab &x) {
+      k_fold_counters<<<1, 32, 0, s>>>(x.cnt);  // warp_add replicas first
+      g_launches++;
+      b.push_back(x.cnt);
+    });
     T.allreduce_sum_u64(b, 11);  // C_VT .. C_BAD_BOUND
   }
 
