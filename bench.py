@@ -433,6 +433,29 @@ def main():
                           f"{ro.iters} iters"),
                "host_cores": host_cores(), "cpu": cpu_model()}
 
+    # ---------------- per-pass %HBM: algorithmic bytes of a pass
+    # = 8.25 V (stencil: g + packed ref read, mark bit) + 14 E_t (edits) +
+    # 8 |S| (R4); the C3 link-walk bytes are left out (a lower bound).  T_iter =
+    # the pass's GPU span (CUDA events, exactz_iter_stats.ms).
+    per_pass = None
+    if not sharded and getattr(r, "pass_ms", None):
+        pk_meas, _ = peaks()
+        ms_l = [t for t in r.pass_ms if t > 0]
+        balg = [8.25 * V + 14.0 * row[1] + 8.0 * r.n_saddles for row in r.stats][:len(ms_l)]
+        fr = sorted(b / (t / 1e3) / 1e9 for b, t in zip(balg, ms_l))
+        tot = sum(balg) / (sum(ms_l) / 1e3) / 1e9
+        per_pass = {"passes": len(ms_l), "ms_min": min(ms_l), "ms_median": statistics.median(ms_l),
+                    "ms_max": max(ms_l), "n_saddles": r.n_saddles,
+                    "alg_bytes": "8.25 V + 14 E_t + 8 |S| per pass (SURVEY 8(d); C3 walks omitted)",
+                    "GBps_median_pass": statistics.median(fr), "GBps_full_run": tot,
+                    "frac_of_8TBs_median_pass": statistics.median(fr) / 8000.0,
+                    "frac_of_measured_median_pass": statistics.median(fr) / pk_meas,
+                    "frac_of_8TBs_full_run": tot / 8000.0,
+                    "passes_at_40pct_of_8TBs": sum(1 for x in fr if x >= 3200.0),
+                    "note": "change tracking re-evaluates only St(edited) u fired vertices, so "
+                            "late passes exceed the dense-pass bytes/time; dense passes are "
+                            "issue-bound (roofline.ncu)"}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
@@ -448,6 +471,7 @@ def main():
                        "edit_pct": None},
             "iterations": iters,
             "hbm_frac": roofline["frac"],
+            "per_pass": per_pass,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": 4.0 * V / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",

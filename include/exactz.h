@@ -92,6 +92,8 @@ typedef struct {
                           (R7 flipped adjacent critical points when REFORMULATED),
                           R6 split events */
   uint64_t walk_steps; /* reserved for diagnostics (0 in this build) */
+  double ms;           /* GPU span of the pass on `stream` (CUDA events; exactz_correct
+                          only, 0 elsewhere): detection, edits and the counter read */
 } exactz_iter_stats;
 
 typedef struct {
@@ -104,6 +106,8 @@ typedef struct {
   double kernel_ms[EXACTZ_K_CLASSES];       /* CUDA-event time on `stream` */
   uint64_t kernel_launches[EXACTZ_K_CLASSES];
   uint64_t kernel_bytes[EXACTZ_K_CLASSES];  /* algorithmic bytes */
+  uint64_t n_saddles;      /* out: |S|, f-saddles (O7; exactz_correct only) */
+  uint64_t n_join, n_split; /* out: |J|, |P| */
 } exactz_stats;
 
 typedef struct {

@@ -27,14 +27,15 @@ if not os.path.exists(LIB_PATH):
 
 class IterStats(C.Structure):
     _fields_ = [("violations", C.c_uint64), ("applied", C.c_uint64), ("n", C.c_uint64 * 6),
-                ("walk_steps", C.c_uint64)]
+                ("walk_steps", C.c_uint64), ("ms", C.c_double)]
 
 
 class Stats(C.Structure):
     _fields_ = [("rows", C.POINTER(IterStats)), ("cap", C.c_uint32), ("nrows", C.c_uint32),
                 ("ms_setup", C.c_double), ("ms_loop", C.c_double),
                 ("kernel_ms", C.c_double * 8), ("kernel_launches", C.c_uint64 * 8),
-                ("kernel_bytes", C.c_uint64 * 8)]
+                ("kernel_bytes", C.c_uint64 * 8), ("n_saddles", C.c_uint64),
+                ("n_join", C.c_uint64), ("n_split", C.c_uint64)]
 
 
 class Opts(C.Structure):
@@ -158,6 +159,8 @@ def _result(status, iters, st, rows):
                                 int(st.kernel_bytes[k])) for k in range(8)}
     res = CorrectResult(status, iters.value, table, st.ms_setup, st.ms_loop, kern)
     res.walk_steps = walks
+    res.pass_ms = [float(r.ms) for r in rows[:n]] if st.cap else []
+    res.n_saddles, res.n_join, res.n_split = int(st.n_saddles), int(st.n_join), int(st.n_split)
     return res
 
 

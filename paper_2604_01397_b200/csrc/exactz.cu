@@ -706,6 +706,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   }();
   unsigned long long prev_vt = (unsigned long long)V;
   const bool allow_track = !(flags & EXACTZ_NO_TRACK);
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pass_ev;
   for (;;) {
     bool may_edit = !(max_iters && it >= max_iters);
     const int round = (int)rows + 1;  // stamps are 16-bit pass numbers
@@ -737,8 +738,19 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       CK(cudaEventCreate(&tb));
       CK(cudaEventRecord(ta, s));
     }
+    // per-pass GPU span for the stats rows (events read after the final sync)
+    cudaEvent_t pa = nullptr, pb = nullptr;
+    if (stats && stats->rows && rows < stats->cap) {
+      CK(cudaEventCreate(&pa));
+      CK(cudaEventCreate(&pb));
+      CK(cudaEventRecord(pa, s));
+    }
     PassOut o = detect_and_edit(C, R, f, out, c, marks, slots, lm, eps, delta, N, flags, may_edit,
                                 tracked ? &trk : nullptr, round);
+    if (pa) {
+      CK(cudaEventRecord(pb, s));
+      pass_ev.push_back({pa, pb});
+    }
     if (tl) {  // GPU span of the pass (main stream) vs host wall-clock span
       CK(cudaEventRecord(tb, s));
       CK(cudaEventSynchronize(tb));
@@ -757,6 +769,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       r.applied = o.applied;
       for (int k = 0; k < 6; ++k) r.n[k] = o.n[k];
       r.walk_steps = o.walk;
+      r.ms = 0.0;  // set from the pass events after the final sync
     }
     ++rows;
     if (o.vt == 0) break;
@@ -782,11 +795,23 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     stats->ms_setup = a;
     stats->ms_loop = b;
     stats->nrows = rows;
+    stats->n_saddles = (uint64_t)R.nS;
+    stats->n_join = (uint64_t)R.nJ;
+    stats->n_split = (uint64_t)R.nP;
+    for (size_t k = 0; k < pass_ev.size(); ++k) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pass_ev[k].first, pass_ev[k].second);
+      stats->rows[k].ms = ms;
+    }
     for (int k = 0; k < EXACTZ_K_CLASSES; ++k) {
       stats->kernel_ms[k] = C.prof.ms[k];
       stats->kernel_launches[k] = C.prof.launches[k];
       stats->kernel_bytes[k] = C.prof.bytes[k];
     }
+  }
+  for (auto &e : pass_ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -884,6 +909,7 @@ exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3]
       row->applied = 0;
       for (int k = 0; k < 6; ++k) row->n[k] = o.n[k];
       row->walk_steps = o.walk;
+      row->ms = 0.0;
     }
     CK(cudaStreamSynchronize(s));
     return EXACTZ_OK;

@@ -272,3 +272,17 @@ def test_parity_compacted_passes(exactz, oracle, cfg, shape):
     (nx not a multiple of 32, ny not of 8): bit-exact with the oracle."""
     f, g, xi = S.make(cfg, shape=shape)
     assert_parity(*run_both(exactz, oracle, f, g, xi, gpu_flags=0x400))
+
+
+@pytest.mark.parametrize("cfg,shape", [("C3", (24, 19, 66)), ("C4", (1, 90, 300))])
+def test_stats_pass_spans_and_saddle_counts(exactz, oracle, cfg, shape):
+    """exactz_stats: |S|, |J|, |P| equal the oracle's reference lists (O7);
+    one positive GPU span per pass, together within the loop's span."""
+    f, g, xi = S.make(cfg, shape=shape)
+    ref = oracle.reference(f.numpy())
+    r = exactz.exactz_correct(f.cuda(), g.cuda(), xi, stats_cap=4096)
+    torch.cuda.synchronize()
+    assert (r.n_saddles, r.n_join, r.n_split) == (len(ref["S"]), len(ref["J"]), len(ref["P"]))
+    assert len(r.pass_ms) == len(r.stats) == r.iters + 1
+    assert all(t > 0 for t in r.pass_ms)
+    assert sum(r.pass_ms) <= r.ms_loop * 1.01 + 0.05
