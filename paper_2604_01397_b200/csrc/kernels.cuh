@@ -97,8 +97,17 @@ __device__ __forceinline__ int div_W(int n, const GridP &G) {  // mark-bitmap ro
 //      bslot[b] = pass in which a steepest slot inside b changed;
 //    a saddle's cached C3 result is reused while no brick its walks touched
 //    changed.
-constexpr int BX = 32, BY = 8, BZ = 8;
-constexpr int SB = 4;  // superbrick = 4 x 4 x 4 bricks (128 x 32 x 32 vertices)
+#ifndef EXACTZ_BY
+#define EXACTZ_BY 8
+#endif
+#ifndef EXACTZ_BZ
+#define EXACTZ_BZ 8
+#endif
+#ifndef EXACTZ_SB
+#define EXACTZ_SB 4
+#endif
+constexpr int BX = 32, BY = EXACTZ_BY, BZ = EXACTZ_BZ;  // BX = one warp row of the stencils
+constexpr int SB = EXACTZ_SB;  // superbrick = SB^3 bricks (4: 128 x 32 x 32 vertices)
 struct Track {
   uint16_t *bval, *bslot;       // brick stamps (nullptr: C3 cache off)
   uint16_t *sbval, *sbslot;     // superbrick stamps (max over its bricks)
@@ -880,8 +889,9 @@ __global__ void __launch_bounds__(NT, 5) k_stencil_compact(const float *__restri
     }
     if (prefetch) store_plane_regs(sg[pz & 3], pre);
     if (T.bval) {
-      if (__syncthreads_or(schg) && tid == 0)
-        stamp(T.bslot, T.sbslot, T, bx, y0 / BY, z / BZ, (uint16_t)T.round);
+      if (__syncthreads_or(schg) && tid == 0)  // every brick the CTA's rows cover
+        for (int b = y0 / BY, bl = (min(y0 + TY, G.ny) - 1) / BY; b <= bl; ++b)
+          stamp(T.bslot, T.sbslot, T, bx, b, z / BZ, (uint16_t)T.round);
     } else {
       __syncthreads();
     }
