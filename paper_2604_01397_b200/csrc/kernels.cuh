@@ -1441,6 +1441,10 @@ __device__ __forceinline__ unsigned events_group(
 // (reference); two walks are in flight per lane (independent loads), each
 // taking the next slot of the set when it finishes.  Pointer steps decode a
 // nibble through a 16-entry shared table of linear offsets (kSelf -> 0).
+#ifndef EXACTZ_EV_KW
+#define EXACTZ_EV_KW 4  // walks in flight per thread (k_events)
+#endif
+
 template <bool UP, bool FROM_REF>
 __device__ __forceinline__ int next_slot(int w, const uint8_t *__restrict__ slots,
                                          const uint32_t *__restrict__ ref) {
@@ -1484,49 +1488,48 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
     }
     int best = -1;
     float bv = 0.0f;
-    constexpr int KW = 4;  // walks in flight per thread (the walks are latency chains)
+    // KW walks in flight per thread (independent loads).  The walks are bound
+    // by the instructions issued per step, so a step is kept to: the slot
+    // load, its nibble, the offset lookup (soff[kSelf] = 0: a root stays put)
+    // and the root test; refills run only when a walk has ended.
+    constexpr int KW = EXACTZ_EV_KW;
+    constexpr unsigned kAll = (1u << KW) - 1u;
     int w[KW];
-    bool run[KW];
+    unsigned runm = 0;  // bit j: walk j in flight
 #pragma unroll
-    for (int j = 0; j < KW; ++j) {
-      w[j] = 0;
-      run[j] = false;
-    }
+    for (int j = 0; j < KW; ++j) w[j] = 0;
     for (;;) {
+      if (runm != kAll && todo) {
 #pragma unroll
-      for (int j = 0; j < KW; ++j)
-        if (!run[j] && todo) {
-          w[j] = s + soff[__ffs(todo) - 1];
-          todo &= todo - 1;
-          run[j] = true;
-        }
-      bool anyrun = false;
-#pragma unroll
-      for (int j = 0; j < KW; ++j) anyrun |= run[j];
-      if (!anyrun) break;
+        for (int j = 0; j < KW; ++j)
+          if (!((runm >> j) & 1u) && todo) {
+            w[j] = s + soff[__ffs(todo) - 1];
+            todo &= todo - 1;
+            runm |= 1u << j;
+          }
+      }
+      if (!runm) break;
       int sv[KW];
-      bool ex[KW];
 #pragma unroll
       for (int j = 0; j < KW; ++j) {
-        sv[j] = 0;
-        ex[j] = false;
-        if (run[j]) {
-          if (SLAB && (w[j] < lo || w[j] >= hi)) ex[j] = true;
-          else sv[j] = next_slot<SPLIT, FROM_REF>(w[j], slots, ref);
+        sv[j] = kSelf;
+        if ((runm >> j) & 1u) {
+          if (!SLAB || (w[j] >= lo && w[j] < hi)) sv[j] = next_slot<SPLIT, FROM_REF>(w[j], slots, ref);
+          else sv[j] = -1;  // sharded: the exit into a neighbour's slab
         }
       }
 #pragma unroll
       for (int j = 0; j < KW; ++j) {
-        if (!run[j]) continue;
-        if (!ex[j] && sv[j] != kSelf) {
+        if (sv[j] >= 0 && sv[j] != kSelf) {
           w[j] += soff[sv[j]];
           continue;
         }
+        if (!((runm >> j) & 1u)) continue;
         // a root (or, sharded, the exit into a neighbour's slab)
-        run[j] = false;
+        runm &= ~(1u << j);
         int lab;
         float val;
-        if (!SLAB || !ex[j]) {
+        if (!SLAB || sv[j] >= 0) {
           lab = w[j] + off;
           val = h[w[j]];
         } else {
