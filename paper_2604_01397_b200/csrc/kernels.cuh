@@ -1304,15 +1304,17 @@ constexpr unsigned long long kFar = 1ull << 63;
 
 __device__ __forceinline__ void brick_bit(int x, int y, int z, int bsx, int bsy, int bsz,
                                           unsigned long long &mask) {
-  const int bx = x / BX, by = y / BY, bz = z / BZ;
-  const int dx = bx - bsx, dy = by - bsy, dz = bz - bsz;
-  if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) {
-    mask |= 1ull << ((dz + 1) * 9 + (dy + 1) * 3 + (dx + 1));
+  // every caller passes in-domain coordinates (>= 0): unsigned shifts
+  const unsigned bx = (unsigned)x / BX, by = (unsigned)y / BY, bz = (unsigned)z / BZ;
+  const unsigned dx = bx - bsx + 1u, dy = by - bsy + 1u, dz = bz - bsz + 1u;  // 0..2: near
+  if (dx <= 2u && dy <= 2u && dz <= 2u) {
+    mask |= 1ull << (dz * 9u + dy * 3u + dx);
     return;
   }
-  const int ex = bx / SB - bsx / SB, ey = by / SB - bsy / SB, ez = bz / SB - bsz / SB;
-  if (ex >= -1 && ex <= 1 && ey >= -1 && ey <= 1 && ez >= -1 && ez <= 1)
-    mask |= 1ull << (32 + (ez + 1) * 9 + (ey + 1) * 3 + (ex + 1));
+  const unsigned ex = bx / SB - (unsigned)bsx / SB + 1u, ey = by / SB - (unsigned)bsy / SB + 1u,
+                 ez = bz / SB - (unsigned)bsz / SB + 1u;
+  if (ex <= 2u && ey <= 2u && ez <= 2u)
+    mask |= 1ull << (32u + ez * 9u + ey * 3u + ex);
   else
     mask |= kFar;
 }
@@ -1683,27 +1685,28 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
     int best = -1;
     float bv = 0.0f;
     int w[2] = {0, 0}, x[2] = {0, 0}, y[2] = {0, 0}, z[2] = {0, 0};
-    bool run[2] = {false, false};
+    unsigned runm = 0;  // bit j: walk j in flight (refills only after a walk ends, as k_events)
     for (;;) {
+      if (runm != 3u && rest) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
-        if (!run[j] && rest) {
-          const int q = __ffs(rest) - 1, p = sdel[q];
-          rest &= rest - 1;
-          w[j] = s + soff[q];
-          x[j] = sx + (p & 3) - 1;
-          y[j] = sy + ((p >> 2) & 3) - 1;
-          z[j] = sz + (p >> 4) - 1;
-          run[j] = true;
-        }
-      if (!run[0] && !run[1]) break;
+        for (int j = 0; j < 2; ++j)
+          if (!((runm >> j) & 1u) && rest) {
+            const int q = __ffs(rest) - 1, p = sdel[q];
+            rest &= rest - 1;
+            w[j] = s + soff[q];
+            x[j] = sx + (p & 3) - 1;
+            y[j] = sy + ((p >> 2) & 3) - 1;
+            z[j] = sz + (p >> 4) - 1;
+            runm |= 1u << j;
+          }
+      }
+      if (!runm) break;
       int sv[2];
 #pragma unroll
       for (int j = 0; j < 2; ++j)
-        sv[j] = run[j] ? (__ldg(&slots[w[j]]) >> (SPLIT ? 4 : 0)) & 15 : 0;
+        sv[j] = ((runm >> j) & 1u) ? (__ldg(&slots[w[j]]) >> (SPLIT ? 4 : 0)) & 15 : kSelf;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        if (!run[j]) continue;
         if (sv[j] != kSelf) {
           const int p = sdel[sv[j]];
           w[j] += soff[sv[j]];
@@ -1713,7 +1716,8 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
           brick_bit(x[j], y[j], z[j], bsx, bsy, bsz, mask);
           continue;
         }
-        run[j] = false;
+        if (!((runm >> j) & 1u)) continue;
+        runm &= ~(1u << j);
         const int lab = w[j];
         const float val = h[lab];
         bool take;
