@@ -1617,15 +1617,29 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
       }
     }
   }
-  // warp-aggregated append of the saddles to recompute
+  // CTA-aggregated append of the saddles to recompute: one atomic per CTA
+  // (per warp, the same-address atomics queued at one L2 slice)
+  __shared__ int wcnt[8], wbase[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned need = __ballot_sync(0xffffffffu, k < n && !valid);
-  if (need) {
-    const int lane = threadIdx.x & 31, leader = __ffs(need) - 1;
+  if (lane == 0) wcnt[wid] = __popc(need);
+  __syncthreads();
+  if (wid == 0) {
+    const int c = lane < 8 ? wcnt[lane] : 0;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, inc, 7);
     int base = 0;
-    if (lane == leader) base = atomicAdd(ntodo, __popc(need));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if ((need >> lane) & 1u) todo[base + __popc(need & ((1u << lane) - 1u))] = k;
+    if (lane == 0 && tot) base = atomicAdd(ntodo, tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane < 8) wbase[lane] = base + inc - c;
   }
+  __syncthreads();
+  if ((need >> lane) & 1u) todo[wbase[wid] + __popc(need & ((1u << lane) - 1u))] = k;
   warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
 }
 
