@@ -1440,7 +1440,7 @@ __device__ __forceinline__ unsigned events_group(
 // Same rules, one lane per saddle (the walks are short: a few steps on
 // average, so per-lane serial walks keep the issue cost per saddle low).  The
 // walk set comes from the stencil's link masks at s (g) or from the f values
-// (reference); two walks are in flight per lane (independent loads), each
+// (reference); EXACTZ_EV_KW walks are in flight per lane (independent loads), each
 // taking the next slot of the set when it finishes.  Pointer steps decode a
 // nibble through a 16-entry shared table of linear offsets (kSelf -> 0).
 #ifndef EXACTZ_EV_KW
