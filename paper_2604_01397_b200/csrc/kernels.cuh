@@ -61,6 +61,11 @@ struct GridP {
   int zb, ze;         // owned local planes [zb, ze)
   uint32_t mnx, mny, mW;  // division by nx, ny, W: q = (umulhi(n, m) + n) >> l (n < 2^31)
   int lnx, lny, lW;
+  // k_stencil_fast key tags as run-time values: (bits & keymask) | tag[k] is
+  // one LOP3 with the tag as a constant-bank operand (with both as
+  // immediates ptxas emits two)
+  uint32_t keymask;   // ~15u
+  uint32_t tag[16];   // tag[k] = k
 };
 
 // Magic numbers of the unsigned division n / d for n < 2^31, d >= 1
@@ -71,6 +76,8 @@ inline void fastdiv_magic(uint32_t d, uint32_t &m, int &l) {
   m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
 }
 inline void grid_fastdiv(GridP &G) {
+  G.keymask = ~15u;
+  for (int k = 0; k < 16; ++k) G.tag[k] = (uint32_t)k;
   fastdiv_magic((uint32_t)G.nx, G.mnx, G.lnx);
   fastdiv_magic((uint32_t)G.ny, G.mny, G.lny);
   fastdiv_magic((uint32_t)G.W, G.mW, G.lW);

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
   const bool inside = x < G.nx && y < G.ny;
   const int c = (ty + 1) * SX + tx + 1;
   const uint32_t vxy = valid_xy(x, y, G);
+  const uint32_t ptx = 1u << tx;  // mark-row placement multiplier (see the row masks)
   unsigned n1 = 0, n2 = 0, n3 = 0;
   const int A = G.nx * G.ny;
 
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
       // argmax / argmin by position-tagged keys, verified against the exact trees
       int q[15];
 #pragma unroll
-      for (int k = 0; k < 15; ++k) q[k] = (int)((bv[k] & ~15u) | (uint32_t)k);
+      for (int k = 0; k < 15; ++k) q[k] = (int)((bv[k] & G.keymask) | G.tag[k]);
       const int qmax = imax3(imax3(imax3(q[0], q[1], q[2]), imax3(q[3], q[4], q[5]),
                                    imax3(q[6], q[7], q[8])),
                              imax3(q[9], q[10], q[11]), imax3(q[12], q[13], q[14]));
@@ -260,8 +261,11 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
       for (int k = 0; k < KR; ++k) {
         constexpr int kStart[KR] = {0, 2, 4, 6, 9, 11, 13};
         const uint32_t cb = ((t >> kStart[k]) & (k == 3 ? 7u : 3u)) << (k >= 4 ? 1 : 0);
-        const uint32_t lo = __reduce_or_sync(0xffffffffu, cb << tx);
-        const uint32_t hi = __reduce_or_sync(0xffffffffu, tx >= 30 ? cb >> (32 - tx) : 0u);
+        // cb << tx and the bits it shifts out (cb <= 7: only lanes 30, 31
+        // carry) as the low and high words of cb * 2^tx, on the FMA pipe
+        // (IMAD / IMAD.HI) instead of three ALU shifts and a select
+        const uint32_t lo = __reduce_or_sync(0xffffffffu, cb * ptx);
+        const uint32_t hi = __reduce_or_sync(0xffffffffu, __umulhi(cb, ptx));
         rv[k] = (u64)lo | ((u64)hi << 32);
       }
     }
