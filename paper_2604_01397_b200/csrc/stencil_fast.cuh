@@ -57,6 +57,30 @@ __device__ __forceinline__ float pos01(float d) {
   return __saturatef(__fmul_rn(__fmul_rn(d, 0x1p126f), 0x1p126f));
 }
 
+// flush_plane (kernels.cuh) for the packed ring of k_stencil_fast: row k of
+// a writer = low word k | carry nibble k of word 7 above bit 32
+__device__ __forceinline__ void flush_plane_packed(uint32_t *__restrict__ marks,
+                                                   const uint32_t (*wr)[TY][8], int p, int z0,
+                                                   int z1, int x0, int y0, const GridP &G) {
+  const int ly = threadIdx.x;
+  if (ly >= SY) return;
+  u64 val = 0;
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const int w = ly - 1 - kr_dy(k), st = p - kr_dz(k);
+    if (w >= 0 && w < TY && st >= z0 && st < z1)
+      val |= (u64)wr[st & 3][w][k] | ((u64)((wr[st & 3][w][7] >> (4 * k)) & 15u) << 32);
+  }
+  const int gy = y0 - 1 + ly;
+  if (!val || gy < 0 || gy >= G.ny || p < 0 || p >= G.nz) return;
+  uint32_t *row = marks + (size_t)(gy + G.ny * p) * G.W;
+  const int wx = x0 >> 5;
+  const uint32_t w = (uint32_t)(val >> 1);
+  if (w) atomicOr(&row[wx], w);
+  if ((val & 1ull) && x0 > 0) atomicOr(&row[wx - 1], 0x80000000u);
+  if (((val >> 33) & 1ull) && x0 + 32 < G.nx) atomicOr(&row[wx + 1], 1u);
+}
+
 template <bool TRACK, bool LALU = false>
 __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict__ g,
                                                         const uint32_t *__restrict__ ref,
@@ -66,7 +90,7 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
                                                         int zc, Track T,
                                                         unsigned long long *cnt) {
   __shared__ uint32_t sb[4][SP];  // staged value bits, 4-plane ring
-  __shared__ __align__(16) u64 wr[4][TY][8];  // mark rows by writer (k_stencil)
+  __shared__ __align__(16) uint32_t wr[4][TY][8];  // mark rows by writer: 7 low words + packed carries
   __shared__ int stab[4][16];     // per z mod 4: star position -> word offset from the centre cell
   __shared__ uint8_t sslot[16];   // star position -> slot code
   const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
@@ -254,28 +278,30 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
     // warp-aggregated mark rows (as k_stencil): the targets re-indexed in
     // ascending linear order put each (dz, dy) row's 2-3 slots on adjacent
     // bits; one OR-reduction per 32-bit half builds the 34-bit row
-    u64 rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (__any_sync(0xffffffffu, tgt)) {
       const uint32_t t = (tgt & 0x7Fu) | ((tgt & 0x3F80u) << 1) | ((tgt >> kSelf) << 7);
+      uint32_t hp = 0;  // the rows' carry-outs, 4 bits per row
 #pragma unroll
       for (int k = 0; k < KR; ++k) {
         constexpr int kStart[KR] = {0, 2, 4, 6, 9, 11, 13};
         const uint32_t cb = ((t >> kStart[k]) & (k == 3 ? 7u : 3u)) << (k >= 4 ? 1 : 0);
         // cb << tx and the bits it shifts out (cb <= 7: only lanes 30, 31
-        // carry) as the low and high words of cb * 2^tx, on the FMA pipe
-        // (IMAD / IMAD.HI) instead of three ALU shifts and a select
-        const uint32_t lo = __reduce_or_sync(0xffffffffu, cb * ptx);
-        const uint32_t hi = __reduce_or_sync(0xffffffffu, __umulhi(cb, ptx));
-        rv[k] = (u64)lo | ((u64)hi << 32);
+        // carry, <= 3 bits) as the low and high words of cb * 2^tx, on the
+        // FMA pipe (IMAD / IMAD.HI); the carries of the 7 rows share one
+        // OR-reduction (packed by IMAD: disjoint nibbles)
+        rv[k] = __reduce_or_sync(0xffffffffu, cb * ptx);
+        hp = __umulhi(cb, ptx) * (1u << (4 * k)) + hp;
       }
+      rv[7] = __reduce_or_sync(0xffffffffu, hp);
     }
     if (tx == 0) {
-      ulonglong2 *d = reinterpret_cast<ulonglong2 *>(&wr[z & 3][ty][0]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) d[k] = make_ulonglong2(rv[2 * k], rv[2 * k + 1]);
+      uint4 *d = reinterpret_cast<uint4 *>(&wr[z & 3][ty][0]);
+      d[0] = make_uint4(rv[0], rv[1], rv[2], rv[3]);
+      d[1] = make_uint4(rv[4], rv[5], rv[6], rv[7]);
     }
     const int pf = z - 2;
-    if (ty == (z & (TY - 1)) && pf >= z0 - 1 && pf >= 0) flush_plane(marks, wr, pf, z0, z1, x0, y0, G);
+    if (ty == (z & (TY - 1)) && pf >= z0 - 1 && pf >= 0) flush_plane_packed(marks, wr, pf, z0, z1, x0, y0, G);
     if (prefetch) store(pz, pre);
     rc = rn;
     pc = pn;
@@ -284,7 +310,7 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
   }
   {
     const int pf = z1 - 2 + ty;
-    if (ty < 3 && pf >= z0 - 1 && pf >= 0 && pf < G.nz) flush_plane(marks, wr, pf, z0, z1, x0, y0, G);
+    if (ty < 3 && pf >= z0 - 1 && pf >= 0 && pf < G.nz) flush_plane_packed(marks, wr, pf, z0, z1, x0, y0, G);
   }
 
   warp_add(&cnt[C_N1 + 0], n1);
