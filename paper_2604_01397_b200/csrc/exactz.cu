@@ -653,9 +653,13 @@ static void validate_inputs(Ctx &C, const float *f, const float *g, float xi,
   }
 }
 
+// g_ready (exactz_correct_host): an event recorded after g_in's host->device
+// copy, which may still be running when the call starts; the reference of f
+// (after a finiteness check of f alone) then overlaps that copy, and the full
+// validation waits for it.
 static exactz_status correct_impl(const float *f, const float *g_in, const int64_t dims[3],
                                   float eps, float *out, uint32_t *iters, const exactz_opts *opts,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, cudaEvent_t g_ready = nullptr) {
   int64_t V = 0;
   if (!f || !g_in || !out || !iters) return EXACTZ_EINVAL;
   if (check_dims(dims, &V) != EXACTZ_OK) return EXACTZ_EINVAL;
@@ -675,10 +679,27 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   CK(cudaEventCreate(&e1));
   CK(cudaEventCreate(&e2));
   CK(cudaEventRecord(e0, s));
-  validate_inputs(C, f, g_in, eps, flags);
-  if (out != g_in) CK(cudaMemcpyAsync(out, g_in, V * sizeof(float), cudaMemcpyDeviceToDevice, s));
   Reference R;
-  build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
+  if (g_ready) {
+    // f alone first (k_validate of (f, f) flags exactly the non-finite f),
+    // its reference while g_in is still in flight, then the full check
+    C.zero();
+    C.run(EXACTZ_K_VALIDATE, 4 * (uint64_t)C.V, true,
+          [&] { k_validate<<<blocks_for(C.V, 256), 256, 0, C.s>>>(f, f, C.V, 0.0f, C.cnt); });
+    C.read();
+    if (C.hcnt[C_BAD_NF]) {
+      set_err("validate", "non-finite value in f or g");
+      throw Error{EXACTZ_EINVAL};
+    }
+    build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
+    CK(cudaStreamWaitEvent(s, g_ready, 0));
+    validate_inputs(C, f, g_in, eps, flags);
+    if (out != g_in) CK(cudaMemcpyAsync(out, g_in, V * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  } else {
+    validate_inputs(C, f, g_in, eps, flags);
+    if (out != g_in) CK(cudaMemcpyAsync(out, g_in, V * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
+  }
   uint8_t *c = (opts && opts->edit_counts) ? opts->edit_counts : C.arena.get<uint8_t>(V);
   uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
   uint8_t *slots = C.arena.get<uint8_t>(V);
@@ -861,14 +882,36 @@ exactz_status exactz_correct_host(const float *f_host, const float *g_in_host,
     cudaStream_t s = (cudaStream_t)stream;
     Arena A(s);
     float *df = A.get<float>(V), *dg = A.get<float>(V);
+    // f on the call's stream, g on a side stream behind it (one copy engine
+    // direction: f arrives first); the reference of f overlaps g's copy
+    cudaStream_t cs;
+    cudaEvent_t fdone, gdone;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&fdone, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&gdone, cudaEventDisableTiming));
+    struct Guard {
+      cudaStream_t cs;
+      cudaEvent_t a, b;
+      ~Guard() {
+        cudaStreamSynchronize(cs);
+        cudaStreamDestroy(cs);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+    } guard{cs, fdone, gdone};
     CK(cudaMemcpyAsync(df, f_host, V * sizeof(float), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dg, g_in_host, V * sizeof(float), cudaMemcpyHostToDevice, s));
+    // g's copy starts when f's is done (also orders dg's stream-ordered
+    // allocation on s before its use on cs)
+    CK(cudaEventRecord(fdone, s));
+    CK(cudaStreamWaitEvent(cs, fdone, 0));
+    CK(cudaMemcpyAsync(dg, g_in_host, V * sizeof(float), cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(gdone, cs));
     exactz_opts o{};
     if (opts_host) o = *opts_host;
     if (o.edit_counts) o.edit_counts = A.get<uint8_t>(V);
     if (o.label_min) o.label_min = A.get<int32_t>(V);
     if (o.label_max) o.label_max = A.get<int32_t>(V);
-    exactz_status st = correct_impl(df, dg, dims, eps_abs, dg, iters, &o, s);
+    exactz_status st = correct_impl(df, dg, dims, eps_abs, dg, iters, &o, s, gdone);
     if (st != EXACTZ_OK && st != EXACTZ_ESTUCK) return st;
     CK(cudaMemcpyAsync(out_host, dg, V * sizeof(float), cudaMemcpyDeviceToHost, s));
     if (opts_host && opts_host->edit_counts)

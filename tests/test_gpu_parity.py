@@ -212,6 +212,33 @@ def test_host_entry_matches_device(exactz):
     assert np.array_equal(rh.out.numpy().view(np.uint32), rd.out.cpu().numpy().view(np.uint32))
 
 
+@pytest.mark.parametrize("cfg,shape", [("C2", (20, 24, 131)), ("C3", (24, 19, 66))])
+def test_host_entry_overlapped_copy(exactz, oracle, cfg, shape):
+    """exactz_correct_host overlaps g's copy with the reference of f: same
+    bits as the oracle, and the validation errors still come first (a
+    non-finite f before the reference, a bound violation or a non-finite g
+    after the copy), with the host out untouched."""
+    E = exactz
+    f, g, xi = S.make(cfg, shape=shape)
+    ro = oracle.correct(f.numpy(), g.numpy(), xi, 5)
+    c = torch.empty(f.numel(), dtype=torch.uint8).pin_memory()
+    rh = E.exactz_correct_host(f.pin_memory(), g.pin_memory(), xi, edit_counts=c)
+    assert rh.status == ro.status and rh.iters == ro.iters
+    assert np.array_equal(rh.out.numpy().reshape(-1).view(np.uint32), ro.out.view(np.uint32))
+    assert np.array_equal(c.numpy(), ro.counts)
+    for fb, gb, want in [(f.clone(), g, E.EINVAL), (f, g.clone(), E.EINVAL), (f, g.clone(), E.EBOUND)]:
+        if want == E.EINVAL and fb is not f:
+            fb.view(-1)[7] = float("inf")
+        elif want == E.EINVAL:
+            gb.view(-1)[7] = float("nan")
+        else:
+            gb.view(-1)[11] = fb.view(-1)[11] + 2 * xi
+        out = torch.full_like(g, 7.0).pin_memory()
+        assert E.status_of(E.exactz_correct_host, fb.pin_memory(), gb.pin_memory(), xi,
+                           out=out) == want
+        assert bool((out == 7.0).all())
+
+
 def test_eps_from_relative(exactz):
     f, _, _ = S.make("C1")
     e = exactz.exactz_eps_from_relative(f.cuda(), 1e-2)
