@@ -154,7 +154,8 @@ struct Ctx {
   int zc = 1;
   bool fast = false;                  // every lo >= 0: k_stencil_fast (set by validation)
   unsigned long long *cnt = nullptr;  // device counters
-  unsigned long long *hcnt = nullptr; // pinned host mirror
+  unsigned long long *hcnt = nullptr; // pinned, mapped host mirror
+  unsigned long long *hcnt_dev = nullptr;  // its device alias
   Arena arena;
   explicit Ctx(cudaStream_t st) : s(st), arena(st) {}
   ~Ctx() {
@@ -231,7 +232,11 @@ struct Ctx {
       rgrid = dim3(bx, (unsigned)(rows < by ? rows : by), 1);
     }
     cnt = arena.get<unsigned long long>(C_NALLOC);
-    CK(cudaMallocHost(&hcnt, C_NCOUNTERS * sizeof(unsigned long long)));
+    // mapped: the fold kernel writes the counters straight into host memory,
+    // so a pass's read needs no copy-engine transfer (a bulk D2H of the
+    // result on a side stream would otherwise queue every pass behind it)
+    CK(cudaHostAlloc((void **)&hcnt, C_NCOUNTERS * sizeof(unsigned long long), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void **)&hcnt_dev, hcnt, 0));
     upload_lut();
   }
   // Keep freed stream-ordered memory in the device's default pool between
@@ -257,10 +262,9 @@ struct Ctx {
   size_t mark_words() const { return (size_t)G.ny * G.nz * G.W; }
   void zero() { CK(cudaMemsetAsync(cnt, 0, C_NALLOC * sizeof(unsigned long long), s)); }
   void read() {
-    k_fold_counters<<<1, 32, 0, s>>>(cnt);  // warp_add replicas -> cnt[0 .. C_NCOUNTERS)
+    // warp_add replicas -> cnt[0 .. C_NCOUNTERS), mirrored into hcnt
+    k_fold_counters<<<1, 32, 0, s>>>(cnt, hcnt_dev);
     g_launches++;
-    CK(cudaMemcpyAsync(hcnt, cnt, C_NCOUNTERS * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (prof.on) prof.drain();
   }
@@ -516,8 +520,25 @@ struct Tracking {
       T.act_next = act[cur ^ 1];
       T.edited = pull_stars ? edited : nullptr;
     }
+    T.patch = patch;
+    T.npatch = npatch;
+    T.patch_cap = patch_cap;
     return T;
   }
+  int32_t *patch = nullptr;  // see HostSnap
+  int *npatch = nullptr;
+  int patch_cap = 0;
+};
+
+// exactz_correct_host: once the passes are sparse, the result's D2H copy
+// starts on a side stream while the remaining passes run; the vertices they
+// edit are listed by k_count_edit and patched into the host copy at the end
+// (a vertex not listed was final before the copy began).
+struct HostSnap {
+  float *out_host = nullptr;
+  uint8_t *counts_host = nullptr;  // nullptr: edit counts not requested
+  cudaStream_t cs = nullptr;
+  bool started = false, overflow = false;
 };
 
 // One CheckConstraints pass on g (O8) followed by the count and, when
@@ -659,7 +680,8 @@ static void validate_inputs(Ctx &C, const float *f, const float *g, float xi,
 // validation waits for it.
 static exactz_status correct_impl(const float *f, const float *g_in, const int64_t dims[3],
                                   float eps, float *out, uint32_t *iters, const exactz_opts *opts,
-                                  cudaStream_t s, cudaEvent_t g_ready = nullptr) {
+                                  cudaStream_t s, cudaEvent_t g_ready = nullptr,
+                                  HostSnap *hs = nullptr) {
   int64_t V = 0;
   if (!f || !g_in || !out || !iters) return EXACTZ_EINVAL;
   if (check_dims(dims, &V) != EXACTZ_OK) return EXACTZ_EINVAL;
@@ -759,6 +781,21 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       CK(cudaEventCreate(&tb));
       CK(cudaEventRecord(ta, s));
     }
+    if (hs && !hs->started && trk.act_on && may_edit && prev_vt * 1024 <= (unsigned long long)V) {
+      trk.patch_cap = (int)std::min<int64_t>(V, V / 64 + 4096);
+      trk.patch = C.arena.get<int32_t>(trk.patch_cap);
+      trk.npatch = C.arena.get<int>(1);
+      CK(cudaMemsetAsync(trk.npatch, 0, sizeof(int), s));
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CK(cudaEventRecord(ev, s));
+      CK(cudaStreamWaitEvent(hs->cs, ev, 0));
+      CK(cudaEventDestroy(ev));
+      CK(cudaMemcpyAsync(hs->out_host, out, V * sizeof(float), cudaMemcpyDeviceToHost, hs->cs));
+      if (hs->counts_host)
+        CK(cudaMemcpyAsync(hs->counts_host, c, V, cudaMemcpyDeviceToHost, hs->cs));
+      hs->started = true;
+    }
     // per-pass GPU span for the stats rows (events read after the final sync)
     cudaEvent_t pa = nullptr, pb = nullptr;
     if (stats && stats->rows && rows < stats->cap) {
@@ -801,6 +838,35 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     ++it;
   }
   CK(cudaEventRecord(e2, s));
+  if (hs && hs->started) {  // patch the host copy with the vertices edited since it began
+    int np = 0;
+    CK(cudaMemcpyAsync(&np, trk.npatch, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (np > trk.patch_cap) {
+      hs->overflow = true;  // the caller copies the whole result
+    } else if (np == 0) {
+      CK(cudaStreamSynchronize(hs->cs));
+    } else {
+      float *vals = C.arena.get<float>(np);
+      uint8_t *cnts = hs->counts_host ? C.arena.get<uint8_t>(np) : nullptr;
+      k_gather_patch<<<(np + 255) / 256, 256, 0, s>>>(trk.patch, np, out, hs->counts_host ? c : nullptr,
+                                                       vals, cnts);
+      g_launches++;
+      CK(cudaGetLastError());
+      std::vector<int32_t> hi(np);
+      std::vector<float> hv(np);
+      std::vector<uint8_t> hc(cnts ? np : 0);
+      CK(cudaMemcpyAsync(hi.data(), trk.patch, np * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(hv.data(), vals, np * sizeof(float), cudaMemcpyDeviceToHost, s));
+      if (cnts) CK(cudaMemcpyAsync(hc.data(), cnts, np, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      CK(cudaStreamSynchronize(hs->cs));
+      for (int k = 0; k < np; ++k) {
+        hs->out_host[hi[k]] = hv[k];
+        if (cnts) hs->counts_host[hi[k]] = hc[k];
+      }
+    }
+  }
   // labels of the final field: the last pass ran on it (no edit followed), so
   // `slots` holds its steepest pointers
   if (opts && (opts->label_min || opts->label_max)) {
@@ -911,11 +977,18 @@ exactz_status exactz_correct_host(const float *f_host, const float *g_in_host,
     if (o.edit_counts) o.edit_counts = A.get<uint8_t>(V);
     if (o.label_min) o.label_min = A.get<int32_t>(V);
     if (o.label_max) o.label_max = A.get<int32_t>(V);
-    exactz_status st = correct_impl(df, dg, dims, eps_abs, dg, iters, &o, s, gdone);
+    HostSnap hs;
+    hs.out_host = out_host;
+    hs.counts_host = (opts_host && opts_host->edit_counts) ? opts_host->edit_counts : nullptr;
+    hs.cs = cs;
+    exactz_status st = correct_impl(df, dg, dims, eps_abs, dg, iters, &o, s, gdone, &hs);
     if (st != EXACTZ_OK && st != EXACTZ_ESTUCK) return st;
-    CK(cudaMemcpyAsync(out_host, dg, V * sizeof(float), cudaMemcpyDeviceToHost, s));
-    if (opts_host && opts_host->edit_counts)
-      CK(cudaMemcpyAsync(opts_host->edit_counts, o.edit_counts, V, cudaMemcpyDeviceToHost, s));
+    if (!hs.started || hs.overflow) {
+      CK(cudaStreamSynchronize(cs));  // a partial copy must not land after the full one
+      CK(cudaMemcpyAsync(out_host, dg, V * sizeof(float), cudaMemcpyDeviceToHost, s));
+      if (opts_host && opts_host->edit_counts)
+        CK(cudaMemcpyAsync(opts_host->edit_counts, o.edit_counts, V, cudaMemcpyDeviceToHost, s));
+    }
     if (opts_host && opts_host->label_min)
       CK(cudaMemcpyAsync(opts_host->label_min, o.label_min, V * 4, cudaMemcpyDeviceToHost, s));
     if (opts_host && opts_host->label_max)

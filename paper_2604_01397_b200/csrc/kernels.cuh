@@ -124,6 +124,11 @@ struct Track {
   uint32_t *gS;                 // g at S[k] (value bits), written by the stencils for C2
   int nbx, nby, nbz, round;
   int nsx, nsy;                 // superbrick grid (x, y extents)
+  // exactz_correct_host: vertices edited after the result's D2H copy began
+  // (patched on the host afterwards); nullptr: off
+  int32_t *patch;
+  int *npatch;
+  int patch_cap;
 };
 
 // Outputs of a stencil at an f-saddle i: its g-lower / g-upper link masks
@@ -289,7 +294,16 @@ __device__ __forceinline__ void warp_add(unsigned long long *dst, unsigned v) {
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(dst + (size_t)(1 + r) * kCntStride, (unsigned long long)s);
 }
 
-__global__ void k_fold_counters(unsigned long long *cnt) {
+// values (and edit counts) of the patched vertices, for the host patch
+__global__ void k_gather_patch(const int32_t *__restrict__ idx, int n, const float *__restrict__ g,
+                               const uint8_t *__restrict__ c, float *vals, uint8_t *cnts) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  vals[k] = g[idx[k]];
+  if (c) cnts[k] = c[idx[k]];
+}
+
+__global__ void k_fold_counters(unsigned long long *cnt, unsigned long long *mirror = nullptr) {
   const int X = threadIdx.x;
   if (X >= C_NCOUNTERS) return;
   unsigned long long t = 0;
@@ -297,7 +311,9 @@ __global__ void k_fold_counters(unsigned long long *cnt) {
     t += cnt[r * kCntStride + X];
     cnt[r * kCntStride + X] = 0;
   }
-  cnt[X] += t;
+  t += cnt[X];
+  cnt[X] = t;
+  if (mirror) mirror[X] = t;  // mapped host memory (Ctx::read)
 }
 
 // ordered 32-bit key of a finite float: key order == IEEE order, -0 == +0
@@ -1915,6 +1931,14 @@ __global__ void __launch_bounds__(256, 8) k_count_edit(float *__restrict__ g,
             if (edit_vertex(g, c, f, base + q, xi, delta, N)) e |= 1u << (4 * sub + q);
       }
       ap += __popc(e);
+      if (TRACK && T.patch && e) {
+        const int n = __popc(e);
+        const int k0 = atomicAdd(T.npatch, n);
+        uint32_t m = e;
+        for (int j = 0; j < n; ++j, m &= m - 1)
+          if (k0 + j < T.patch_cap)
+            T.patch[k0 + j] = (int32_t)((size_t)G.nx * row + (size_t)wx * 32 + (__ffs(m) - 1));
+      }
       if (TRACK && (T.bval || T.act_next)) {
         uint32_t E = e;  // OR over the 8 lanes of the word
         E |= __shfl_xor_sync(gmask, E, 1);
