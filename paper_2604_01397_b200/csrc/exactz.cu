@@ -781,7 +781,11 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       CK(cudaEventCreate(&tb));
       CK(cudaEventRecord(ta, s));
     }
-    if (hs && !hs->started && trk.act_on && may_edit && prev_vt * 1024 <= (unsigned long long)V) {
+    static const unsigned long long snap_div = [] {
+      const char *e = std::getenv("EXACTZ_SNAP_DIV");  // tuning knob (default 1024)
+      return e ? std::strtoull(e, nullptr, 10) : 1024ull;
+    }();
+    if (hs && !hs->started && trk.act_on && may_edit && prev_vt * snap_div <= (unsigned long long)V) {
       trk.patch_cap = (int)std::min<int64_t>(V, V / 64 + 4096);
       trk.patch = C.arena.get<int32_t>(trk.patch_cap);
       trk.npatch = C.arena.get<int>(1);
