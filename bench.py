@@ -311,6 +311,23 @@ def main():
         roofline["traffic"] = ent.get("bytes_per_launch")
         roofline["traffic_source"] = tr.get("source")
         roofline["ncu"] = {k: v for k, v in ent.items() if k != "bytes_per_launch"}
+        # the dense stencil is bound by instruction issue, not HBM: its warp-
+        # instructions per launch (ncu, profiles/traffic.json) over the live
+        # launch time, against 148 SMs x 4 schedulers x 1 instr/clk at the
+        # measured SM clock (B200_PROFILING.md unit counts)
+        wi = ent.get("warp_instr_per_32_vertices")
+        if wi and dn and dms:
+            try:
+                mhz = float(json.load(open(MEASURED_PEAKS)).get("sm_max_mhz", 1965.0))
+            except Exception:
+                mhz = 1965.0
+            instr = wi * V / 32.0
+            ach = instr / ((dms / dn) / 1e3) / 1e9
+            pk = 148 * 4 * mhz * 1e6 / 1e9
+            roofline["issue"] = {"bound": "issue", "achieved": ach, "peak": pk,
+                                 "unit": "G warp-instr/s", "frac": ach / pk,
+                                 "warp_instr_per_launch": instr,
+                                 "source": "instructions from ncu (traffic.json), time live"}
     except Exception:
         pass
 
