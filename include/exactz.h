@@ -174,9 +174,18 @@ exactz_status exactz_edit_log(const float *g_in, const float *out, const uint8_t
 
 /* Decode an EXCE stream (buf, bytes: HOST) and apply it to g_in (DEVICE):
  * out (DEVICE, may alias g_in) = g_in with every entry replayed (Stepped) or
- * stored (Lossless).  EXACTZ_EINVAL on a malformed or truncated stream. */
+ * stored (Lossless).  n_elems = the element count of g_in and out; it must
+ * equal nx*ny*nz of the stream's header.  The stream is untrusted input:
+ * EXACTZ_EINVAL on a malformed or truncated stream, a header whose sizes do
+ * not fit `bytes`, an index gap past the end of the field or a dims mismatch,
+ * always before any device write.
+ * Format note: the header is this library's own (64 bytes: magic "EXCE",
+ * version, codec, xi as float32 — the ABI's eps type —, N, the dims, entry
+ * count, payload and raw sizes); SPEC's CPU program writes xi as f64 in a
+ * shorter header, so the two streams are not interchangeable byte for byte
+ * (NEXT-4). */
 exactz_status exactz_edit_log_apply(const uint8_t *buf, uint64_t bytes, const float *g_in,
-                                    float *out, void *stream);
+                                    float *out, int64_t n_elems, void *stream);
 
 /* xi = RN_f32(rel * (max f - min f)) computed in double (amb-19). */
 exactz_status exactz_eps_from_relative(const float *f, int64_t n, double rel, float *eps_abs,

@@ -62,7 +62,7 @@ _lib.exactz_vulnerability.restype = C.c_int
 _lib.exactz_edit_log.argtypes = [_P, _P, _P, _i64p, C.c_float, C.c_uint32, C.c_int, _P,
                                  C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _P]
 _lib.exactz_edit_log.restype = C.c_int
-_lib.exactz_edit_log_apply.argtypes = [_P, C.c_uint64, _P, _P, _P]
+_lib.exactz_edit_log_apply.argtypes = [_P, C.c_uint64, _P, _P, C.c_int64, _P]
 _lib.exactz_edit_log_apply.restype = C.c_int
 _lib.exactz_eps_from_relative.argtypes = [_P, C.c_int64, C.c_double, C.POINTER(C.c_float), _P]
 _lib.exactz_eps_from_relative.restype = C.c_int
@@ -199,7 +199,18 @@ def exactz_correct_host(f, g_in, eps: float, out=None, *, N: int = 5, max_iters:
         if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
             raise ValueError("f and g_in must be contiguous float32 CPU tensors")
     if out is None:
-        out = torch.empty_like(g_in)
+        # pinned like g_in: a D2H copy into pageable memory blocks the host and
+        # cannot overlap the late passes
+        out = torch.empty(g_in.shape, dtype=torch.float32, pin_memory=g_in.is_pinned())
+    V = g_in.numel()
+    if f.numel() != V:
+        raise ValueError("f and g_in differ in size")
+    for name, t, dt in (("out", out, torch.float32), ("edit_counts", edit_counts, torch.uint8),
+                        ("label_min", label_min, torch.int32),
+                        ("label_max", label_max, torch.int32)):
+        if t is not None and (t.is_cuda or t.dtype != dt or not t.is_contiguous()
+                              or t.numel() != V):
+            raise ValueError(f"{name} must be a contiguous {dt} CPU tensor of {V} elements")
     o, st, rows = _opts(N, max_iters, flags, edit_counts, label_min, label_max, stats_cap)
     iters = C.c_uint32(0)
     s = _lib.exactz_correct_host(_ptr(f), _ptr(g_in), _dims(f), float(eps), _ptr(out),
@@ -258,8 +269,11 @@ def exactz_edit_log_apply(log: bytes, g_in, out=None, stream=None):
     import torch
     if out is None:
         out = torch.empty_like(g_in)
+    if out.numel() != g_in.numel():
+        raise ValueError("out and g_in differ in size")
     b = (C.c_uint8 * len(log)).from_buffer_copy(log)
-    s = _lib.exactz_edit_log_apply(b, len(log), _ptr(g_in), _ptr(out), _stream(stream))
+    s = _lib.exactz_edit_log_apply(b, len(log), _ptr(g_in), _ptr(out), g_in.numel(),
+                                   _stream(stream))
     if s != OK:
         raise ExactzError(s, "exactz_edit_log_apply")
     return out

@@ -772,7 +772,13 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
           prev_vt * cache_div <= (unsigned long long)trk.nb)
         trk.start_cache(C, R);
     }
-    const bool tracked = allow_track && round < 65000 && (trk.act_on || trk.cache_on);
+    // (debug 0x40000: passes after the host copy began run untracked, the
+    // path a run beyond round 65000 takes)
+    const bool tracked = allow_track && round < 65000 && (trk.act_on || trk.cache_on) &&
+                         !((flags & 0x40000u) && hs && hs->started);
+    // an untracked pass lists no edits for the host copy's patch: once the
+    // copy has begun, the caller must copy the whole result instead
+    if (hs && hs->started && !tracked) hs->overflow = true;
     static const bool tl = std::getenv("EXACTZ_TIMELINE") != nullptr;  // diagnostic
     cudaEvent_t ta = nullptr, tb = nullptr;
     auto h0 = std::chrono::steady_clock::now();
@@ -785,8 +791,11 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       const char *e = std::getenv("EXACTZ_SNAP_DIV");  // tuning knob (default 1024)
       return e ? std::strtoull(e, nullptr, 10) : 1024ull;
     }();
-    if (hs && !hs->started && trk.act_on && may_edit && prev_vt * snap_div <= (unsigned long long)V) {
-      trk.patch_cap = (int)std::min<int64_t>(V, V / 64 + 4096);
+    // (debug 0x10000: start as soon as vertex activity is on; 0x20000: a
+    // one-entry patch list, so any later edit overflows it)
+    if (hs && !hs->started && trk.act_on && may_edit &&
+        ((flags & 0x10000u) || prev_vt * snap_div <= (unsigned long long)V)) {
+      trk.patch_cap = (flags & 0x20000u) ? 1 : (int)std::min<int64_t>(V, V / 64 + 4096);
       trk.patch = C.arena.get<int32_t>(trk.patch_cap);
       trk.npatch = C.arena.get<int>(1);
       CK(cudaMemsetAsync(trk.npatch, 0, sizeof(int), s));
@@ -846,7 +855,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     int np = 0;
     CK(cudaMemcpyAsync(&np, trk.npatch, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (np > trk.patch_cap) {
+    if (hs->overflow || np > trk.patch_cap) {
       hs->overflow = true;  // the caller copies the whole result
     } else if (np == 0) {
       CK(cudaStreamSynchronize(hs->cs));
@@ -1260,7 +1269,7 @@ exactz_status exactz_edit_log(const float *g_in, const float *out, const uint8_t
 }
 
 exactz_status exactz_edit_log_apply(const uint8_t *buf, uint64_t bytes, const float *g_in,
-                                    float *out, void *stream) {
+                                    float *out, int64_t n_elems, void *stream) {
   return guarded([&]() -> exactz_status {
     if (!buf || !g_in || !out || bytes < sizeof(ExceHeader)) return EXACTZ_EINVAL;
     ExceHeader h;
@@ -1268,8 +1277,13 @@ exactz_status exactz_edit_log_apply(const uint8_t *buf, uint64_t bytes, const fl
     int64_t V = 0;
     const int64_t dims[3] = {h.nx, h.ny, h.nz};
     if (std::memcmp(h.magic, "EXCE", 4) || h.version != 1 || h.codec > 1 || h.N < 1 ||
-        h.N > 254 || check_dims(dims, &V) != EXACTZ_OK || sizeof(h) + h.payload > bytes) {
+        h.N > 254 || check_dims(dims, &V) != EXACTZ_OK || h.payload > bytes - sizeof(h) ||
+        h.entries > (uint64_t)V || h.raw > (uint64_t)V * 15) {
       set_err("exactz_edit_log_apply", "malformed EXCE stream");
+      return EXACTZ_EINVAL;
+    }
+    if (V != n_elems) {
+      set_err("exactz_edit_log_apply", "stream dims do not match the caller's element count");
       return EXACTZ_EINVAL;
     }
     std::vector<uint8_t> raw;
@@ -1309,8 +1323,13 @@ exactz_status exactz_edit_log_apply(const uint8_t *buf, uint64_t bytes, const fl
         sh += 7;
         if (!(b & 0x80)) break;
       }
+      // d <= V - 1 - (prev + 1) keeps i in [0, V) without signed overflow
+      if (prev + 1 >= V || d > (uint64_t)(V - 1 - (prev + 1)) || p >= raw.size()) {
+        set_err("exactz_edit_log_apply", "entry out of range or truncated");
+        return EXACTZ_EINVAL;
+      }
       const int64_t i = prev + 1 + (int64_t)d;
-      if (i >= V || p >= raw.size()) {
+      if (i >= V) {
         set_err("exactz_edit_log_apply", "entry out of range or truncated");
         return EXACTZ_EINVAL;
       }

@@ -342,7 +342,10 @@ struct ShardedRun {
       k_validate<<<blocks_for(x.nzl * P, 256), 256, 0, s>>>(x.f + P, x.g + P, x.nzl * P, xi, x.cnt);
     });
     CK(cudaGetLastError());
-    allreduce_counters();
+    // C_NEG too: every slab must make the single-GPU call's fast/general
+    // stencil choice, which depends on the whole field (the halo planes of a
+    // slab hold a neighbour's values).  The other counters are zero here.
+    allreduce_counters(C_NEG + 1);
     read_counters();
     if (sl[0].hcnt[C_BAD_NF]) {
       set_err("validate", "non-finite value in f or g");
@@ -547,14 +550,16 @@ struct ShardedRun {
     CK(cudaGetLastError());
   }
 
-  void allreduce_counters() {
+  // Sums counters [0, n) over the ranks.  Per pass only C_VT .. C_BAD_BOUND
+  // are global; C_NREMOTE / C_WALK stay per rank.
+  void allreduce_counters(int n = C_BAD_BOUND + 1) {
     std::vector<unsigned long long *> b;
     each([&](Slab &x) {
       k_fold_counters<<<1, 32, 0, s>>>(x.cnt);  // warp_add replicas first
       g_launches++;
       b.push_back(x.cnt);
     });
-    T.allreduce_sum_u64(b, 11);  // C_VT .. C_BAD_BOUND
+    T.allreduce_sum_u64(b, n);
   }
 
   // One CheckConstraints pass (+ edits): returns {V_t, applied, n1..n6}

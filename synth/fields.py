@@ -213,9 +213,35 @@ CONFIGS = {
 _GENS = dict(gaussmix=gaussmix, nyx_like=nyx_like, combustion=combustion, climate2d=climate2d)
 
 
+class _one_thread:
+    """CPU generation pinned to one torch thread: the FFT (MKL) and the
+    reductions (mean, std, max) split their work by thread count, so the
+    bytes of a CPU-generated field depend on it (C2: different SHA-256 at 1
+    and 8 threads).  With one thread the bytes are a function of the seed
+    only, which the full-size goldens (tests/golden/fullsize_*.json) need."""
+
+    def __init__(self, device):
+        self.on = torch.device(device).type == "cpu"
+
+    def __enter__(self):
+        if self.on:
+            self.n = torch.get_num_threads()
+            torch.set_num_threads(1)
+
+    def __exit__(self, *a):
+        if self.on:
+            torch.set_num_threads(self.n)
+
+
 def make(config: str, device="cpu", shape=None, mode: str = "uniform"):
     """(f, ghat, xi) for a config id; `shape` overrides the 3D shape (scaled
-    samples with the same recipe)."""
+    samples with the same recipe).  On the CPU the bytes are host- and
+    thread-count-independent (see _one_thread)."""
+    with _one_thread(device):
+        return _make(config, device, shape, mode)
+
+
+def _make(config, device, shape, mode):
     c = CONFIGS[config]
     kw = dict(c["kw"])
     if shape is not None:
@@ -229,6 +255,4 @@ def make(config: str, device="cpu", shape=None, mode: str = "uniform"):
     f = _GENS[c["gen"]](device=device, **kw)
     xi = xi_from_rel(f, c["rel"])
     g = decompress(f, xi, c["seed"], mode=mode)
-    if f.dim() == 3 and c["gen"] == "climate2d":
-        pass
     return f.contiguous(), g.contiguous(), xi

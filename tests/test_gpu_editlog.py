@@ -67,3 +67,53 @@ def test_edit_log_empty_and_malformed(exactz):
     assert ne > 0
     truncated = log[:-1]
     assert exactz.status_of(exactz.exactz_edit_log_apply, truncated, g) == exactz.EINVAL
+
+
+def test_edit_log_untrusted_streams(exactz):
+    """a varint gap >= 2^63, a payload size that wraps the header
+    sum, and a header whose dims disagree with the caller's buffers are all
+    EXACTZ_EINVAL, before any device write."""
+    import struct
+    f, _, xi = S.make("C1")
+    fd = f.cuda()
+    c = torch.zeros(f.numel(), dtype=torch.uint8, device="cuda")
+    hdr, _ = exactz.exactz_edit_log(fd, fd, c, xi)
+    assert len(hdr) == 64
+    E = exactz
+
+    def with_payload(pay, entries):
+        h = bytearray(hdr)
+        struct.pack_into("<QQQ", h, 40, entries, len(pay), len(pay))
+        return bytes(h) + pay
+
+    # one entry whose gap is 2^63 + 5 (10-byte varint), kind Stepped(1)
+    gap = (1 << 63) + 5
+    vb = bytearray()
+    while True:
+        b = gap & 0x7F
+        gap >>= 7
+        vb.append(b | (0x80 if gap else 0))
+        if not gap:
+            break
+    out = fd.clone()
+    assert E.status_of(E.exactz_edit_log_apply, with_payload(bytes(vb) + b"\x01", 1), fd,
+                       out=out) == E.EINVAL
+    assert torch.equal(out, fd)
+    # gap exactly past the end: V (index V), and V - 1 (the last vertex) is fine
+    V = f.numel()
+    for gap, ok in ((V, False), (V - 1, True)):
+        vb = bytearray()
+        while True:
+            b = gap & 0x7F
+            gap >>= 7
+            vb.append(b | (0x80 if gap else 0))
+            if not gap:
+                break
+        st = E.status_of(E.exactz_edit_log_apply, with_payload(bytes(vb) + b"\x01", 1), fd)
+        assert (st == E.OK) == ok
+    # payload size near 2^64: the header sum would wrap
+    h = bytearray(hdr)
+    struct.pack_into("<QQQ", h, 40, 0, (1 << 64) - 32, (1 << 64) - 32)
+    assert E.status_of(E.exactz_edit_log_apply, bytes(h), fd) == E.EINVAL
+    # dims of the stream (16^3) against a smaller caller buffer
+    assert E.status_of(E.exactz_edit_log_apply, hdr, fd[:8].contiguous()) == E.EINVAL

@@ -313,3 +313,36 @@ def test_stats_pass_spans_and_saddle_counts(exactz, oracle, cfg, shape):
     assert len(r.pass_ms) == len(r.stats) == r.iters + 1
     assert all(t > 0 for t in r.pass_ms)
     assert sum(r.pass_ms) <= r.ms_loop * 1.01 + 0.05
+
+
+SNAP_EARLY, SNAP_CAP1, SNAP_UNTRACK = 0x10000, 0x20000, 0x40000
+
+
+@pytest.mark.parametrize("dbg", [SNAP_EARLY, SNAP_EARLY | SNAP_CAP1, SNAP_EARLY | SNAP_UNTRACK],
+                         ids=["patched", "overflow", "untracked_after_start"])
+def test_host_snapshot_branches(exactz, oracle, dbg):
+    """exactz_correct_host starts the result's D2H copy while passes
+    still run and patches the vertices edited afterwards.  Debug flags force
+    the copy to start at the first list-based pass (patched branch), with a
+    one-entry patch list (overflow: full copy), and with the passes after the
+    start untracked (no patch list: full copy).  Every branch must give the
+    oracle's out and edit counts."""
+    E = exactz
+    f, g, xi = S.make("C2", shape=(30, 40, 70))
+    ro = oracle.correct(f.numpy(), g.numpy(), xi, 5)
+    c = torch.empty(f.numel(), dtype=torch.uint8).pin_memory()
+    rh = E.exactz_correct_host(f.pin_memory(), g.pin_memory(), xi, edit_counts=c, flags=dbg)
+    assert rh.status == ro.status and rh.iters == ro.iters
+    assert rh.out.is_pinned()
+    assert np.array_equal(rh.out.numpy().reshape(-1).view(np.uint32), ro.out.view(np.uint32))
+    assert np.array_equal(c.numpy(), ro.counts)
+
+
+def test_host_entry_rejects_bad_outputs(exactz):
+    f, g, xi = S.make("C1")
+    E = exactz
+    for kw in ({"out": torch.empty(5)}, {"edit_counts": torch.empty(f.numel())},
+               {"label_min": torch.empty(f.numel(), dtype=torch.int64)},
+               {"label_max": torch.empty(f.numel(), dtype=torch.int32, device="cuda")}):
+        with pytest.raises(ValueError):
+            E.exactz_correct_host(f, g, xi, **kw)

@@ -77,3 +77,22 @@ def test_slabs_errors(exactz):
 def test_slabs_reformulated(exactz, p):
     f, g, xi = S.make("C3", shape=(15, 20, 40))
     assert_same(*both(exactz, f, g, xi, p, flags=exactz.REFORMULATED))
+
+
+def test_slabs_negative_values_in_one_slab(exactz, oracle):
+    """Negative values only in the upper slab, starting at the slab border:
+    the lower slab's owned planes are all positive but its ghost plane is not,
+    so the fast (unsigned-key) stencil would be wrong there.  Every slab must
+    make the whole field's fast/general choice (C_NEG reduced over
+    the ranks)."""
+    f, _, _ = S.make("C1")
+    f = f.clone()
+    f[8:] -= 2.5                        # p = 2: slab 1 owns z = 8..15
+    xi = float(np.float32(1e-2 * float(f.max() - f.min())))
+    g = S.decompress(f, xi, 7)
+    assert float(f[:8].min()) > 0 and float(f[8].min()) < 0
+    a, b, c1, c2 = both(exactz, f, g, xi, 2)
+    assert_same(a, b, c1, c2)
+    r = oracle.correct(f.numpy(), g.numpy(), xi, 5)
+    assert b.iters == r.iters and b.status == r.status
+    assert np.array_equal(b.out.cpu().numpy().reshape(-1).view(np.uint32), r.out.view(np.uint32))
