@@ -30,6 +30,10 @@ sys.path.insert(0, ROOT)
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 METRIC = "correction GB/s (field bytes/wall time)"
+KERNELS = {"stencil": "k_stencil_key2 (dense CheckConstraints stencil, R1-R3)",
+           "events": "k_events / k_events_cached (C3 label walks, R5/R6)",
+           "edit": "k_count_edit", "stencil_sparse": "k_act_list + k_stencil_list",
+           "saddle_order": "k_saddle_order_vals (C2, R4)"}
 
 
 def parse():
@@ -159,14 +163,23 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def golden_run(G, V_full):
+    """the cached single-thread oracle run of the whole config (same input
+    SHA-256; tools/make_golden.py), quoted with its host and date"""
+    if not G:
+        return None
+    return {"value": 4.0 * V_full / G["oracle_s"] / 1e9, "unit": "GB/s", "seconds": G["oracle_s"],
+            "iterations": G["iters"], "threads": G.get("oracle_threads", 1),
+            "host_cpu": G.get("host_cpu"), "host_nproc": G.get("host_nproc"), "date": G.get("date"),
+            "source": f"tests/golden/fullsize_{G['config']}.json (tools/make_golden.py)"}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on the box's host cores."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    import torch
-    from synth import fields as S
-    f, g, xi = S.make(args.config, device="cuda" if torch.cuda.is_available() else "cpu")
+    f, g, xi, shas, golden = make_inputs(args.config)
     n = max(16, args.cpu_sample * 3 // 4)
     fs, gs = crop(f, g, n)
     fs, gs = fs.cpu(), gs.cpu()
@@ -186,17 +199,67 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, f) + " (bounded CPU sample)"},
+        "config": {"workload": workload_name(args.config, f) + " (bounded CPU sample)",
+                   "sha256_f": shas["f"], "sha256_ghat": shas["ghat"]},
         "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": sample, "host_cores": host_cores(), "cpu": cpu_model()},
+                         "sample": sample, "host_cores": host_cores(), "cpu": cpu_model(),
+                         "full_run": golden_run(golden, V_full=f.numel())},
         "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N > 1 without torchrun: start N ranks (one per GPU) the way the
+    driver does.  Under torchrun, WORLD_SIZE must equal --gpus."""
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                   f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+            return subprocess.call(cmd)
+        return None
+    if int(ws_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
+    return None
+
+
+def sha256(t) -> str:
+    import hashlib
+    return hashlib.sha256(t.contiguous().cpu().numpy().tobytes()).hexdigest()
+
+
+def make_inputs(cfg):
+    """The config's field and its simulated decompression, generated on the
+    CPU (one torch thread: bytes set by the seed alone, identical on every
+    host), with their SHA-256 and the cached full-size oracle run of the
+    same bytes when tests/golden holds one."""
+    from synth import fields as S
+    f, g, xi = S.make(cfg)
+    shas = {"f": sha256(f), "ghat": sha256(g)}
+    golden = None
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_{cfg}.json")
+    if os.path.exists(path):
+        G = json.load(open(path))
+        if G.get("sha_f") == shas["f"] and G.get("sha_ghat") == shas["ghat"] and "oracle_s" in G:
+            golden = G
+    return f, g, xi, shas, golden
+
+
 def main():
     args = parse()
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -217,7 +280,8 @@ def main():
     import paper_2604_01397_b200 as E
     from synth import fields as S
 
-    f, g, xi = S.make(args.config, device=dev)
+    f, g, xi, shas, golden = make_inputs(args.config)
+    f, g = f.to(dev), g.to(dev)
     V = f.numel()
     wname = workload_name(args.config, f)
     stream = torch.cuda.current_stream()
@@ -277,8 +341,10 @@ def main():
 
     r = results[-1]
     iters = r.iters
-    # roofline of the dominant kernel class (CUDA events on the launch stream;
-    # single-GPU call only: the sharded call does not profile per kernel)
+    # Kernel classes timed with CUDA events on their launch streams
+    # (EXACTZ_PROFILE, separate untimed steps).  algorithmic bytes per
+    # launch: dense stencil 8.25 B per vertex;
+    # C3 events 8 B per saddle walked + 8 B per link vertex walked from.
     agg = {}
     for res in profiled:
         for k, (ms, n, b) in res.kernels.items():
@@ -286,43 +352,47 @@ def main():
             a[0] += ms
             a[1] += n
             a[2] += b
-    # the dominant kernel class among those timed on the main stream (the C3
-    # event kernels run on two side streams; their event-timed spans overlap
-    # each other and are not exclusive times)
-    main = {k: v for k, v in agg.items() if k != "events"}
-    dom = max(main, key=lambda k: main[k][0]) if main else "stencil"
-    dms, dn, dbytes = agg.get(dom, (0.0, 0, 0))
     peak, peak_src = peaks()
-    achieved = (dbytes / dn) / ((dms / dn) / 1e3) / 1e9 if dn and dms else None
-    share = dms / (ms_step * prof_steps)
-    roofline = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                "traffic": None, "peak_source": peak_src,
-                "share_of_step": share,
-                "bytes_per_launch": dbytes / dn if dn else None,
-                "ms_per_launch": dms / dn if dn else None,
-                "classes": {k: {"ms": v[0] / prof_steps, "launches": v[1] / prof_steps,
-                                "GB/s": (v[2] / (v[0] / 1e3) / 1e9) if v[0] else None}
-                            for k, v in agg.items() if v[1]}}
+
+    def roof(cls):
+        ms, n, b = agg.get(cls, (0.0, 0, 0))
+        if not n or not ms:
+            return None
+        ach = (b / n) / ((ms / n) / 1e3) / 1e9
+        return {"bound": "hbm", "kernel": KERNELS.get(cls, cls), "achieved": ach, "peak": peak,
+                "unit": "GB/s", "frac": ach / peak, "traffic": None, "peak_source": peak_src,
+                "bytes_per_launch": b / n, "ms_per_launch": ms / n, "launches_per_step": n / prof_steps,
+                "share_of_step": ms / (ms_step * prof_steps)}
+
+    # the dense stencil: the per-iteration kernel of north_star's 40 % gate and
+    # the dominant kernel on the main stream
+    roofline = roof("stencil") or {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
+                                   "frac": None, "traffic": None}
+    roofline["classes"] = {k: {"ms": v[0] / prof_steps, "launches": v[1] / prof_steps,
+                               "GB/s": (v[2] / (v[0] / 1e3) / 1e9) if v[0] else None}
+                           for k, v in agg.items() if v[1]}
+    roofline_events = roof("events")
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         tr = json.load(open(traffic_path))
-        ent = tr.get(f"k_{dom}", {})
-        roofline["traffic"] = ent.get("bytes_per_launch")
-        roofline["traffic_source"] = tr.get("source")
-        roofline["ncu"] = {k: v for k, v in ent.items() if k != "bytes_per_launch"}
-        # the dense stencil is bound by instruction issue, not HBM: its warp-
-        # instructions per launch (ncu, profiles/traffic.json) over the live
-        # launch time, against 148 SMs x 4 schedulers x 1 instr/clk at the
-        # measured SM clock (B200_PROFILING.md unit counts)
-        wi = ent.get("warp_instr_per_32_vertices")
-        if wi and dn and dms:
+        for key, rl in (("k_stencil", roofline), ("k_events", roofline_events)):
+            ent = tr.get(key, {})
+            if rl is None or not ent:
+                continue
+            rl["traffic"] = ent.get("bytes_per_launch")
+            rl["traffic_source"] = tr.get("source")
+            rl["ncu"] = {k: v for k, v in ent.items() if k != "bytes_per_launch"}
+        # the dense stencil's issue rate: warp-instructions per launch (ncu,
+        # profiles/traffic.json) over the live launch time, against 148 SMs x
+        # 4 schedulers x 1 instr/clk at the measured SM clock
+        wi = tr.get("k_stencil", {}).get("warp_instr_per_32_vertices")
+        if wi and roofline.get("ms_per_launch"):
             try:
                 mhz = float(json.load(open(MEASURED_PEAKS)).get("sm_max_mhz", 1965.0))
             except Exception:
                 mhz = 1965.0
             instr = wi * V / 32.0
-            ach = instr / ((dms / dn) / 1e3) / 1e9
+            ach = instr / (roofline["ms_per_launch"] / 1e3) / 1e9
             pk = 148 * 4 * mhz * 1e6 / 1e9
             roofline["issue"] = {"bound": "issue", "achieved": ach, "peak": pk,
                                  "unit": "G warp-instr/s", "frac": ach / pk,
@@ -448,30 +518,36 @@ def main():
                "sample": (f"centred {'x'.join(str(d) for d in reversed(tuple(fs.shape)))} crop "
                           f"of the same field, xi of the full field; {dt:.1f} s, "
                           f"{ro.iters} iters"),
-               "host_cores": host_cores(), "cpu": cpu_model()}
+               "host_cores": host_cores(), "cpu": cpu_model(),
+               "full_run": golden_run(golden, V)}
 
     # ---------------- per-pass %HBM: algorithmic bytes of a pass
-    # = 8.25 V (stencil: g + packed ref read, mark bit) + 14 E_t (edits) +
-    # 8 |S| (R4); the C3 link-walk bytes are left out (a lower bound).  T_iter =
-    # the pass's GPU span (CUDA events, exactz_iter_stats.ms).
+    # = 8.25 B per vertex the stencil evaluated (V in a dense pass, the active
+    # set in a change-tracked one) + 14 B per edit + 8 B per saddle (R4) + 8 B
+    # per C3 link vertex walked from; T_iter = the pass's GPU span (CUDA
+    # events on the call's stream, exactz_iter_stats.ms).
     per_pass = None
     if not sharded and getattr(r, "pass_ms", None):
         pk_meas, _ = peaks()
-        ms_l = [t for t in r.pass_ms if t > 0]
-        balg = [8.25 * V + 14.0 * row[1] + 8.0 * r.n_saddles for row in r.stats][:len(ms_l)]
-        fr = sorted(b / (t / 1e3) / 1e9 for b, t in zip(balg, ms_l))
+        rows = [(t, e, row[1], lk) for t, e, row, lk in
+                zip(r.pass_ms, r.pass_evaluated, r.stats, r.pass_links) if t > 0]
+        balg = [8.25 * e + 14.0 * ap + 8.0 * r.n_saddles + 8.0 * lk for _, e, ap, lk in rows]
+        ms_l = [t for t, *_ in rows]
+        fr = [b / (t / 1e3) / 1e9 for b, t in zip(balg, ms_l)]
         tot = sum(balg) / (sum(ms_l) / 1e3) / 1e9
+        dense = [x for x, (_, e, _, _) in zip(fr, rows) if e == V]
         per_pass = {"passes": len(ms_l), "ms_min": min(ms_l), "ms_median": statistics.median(ms_l),
                     "ms_max": max(ms_l), "n_saddles": r.n_saddles,
-                    "alg_bytes": "8.25 V + 14 E_t + 8 |S| per pass (SURVEY 8(d); C3 walks omitted)",
+                    "alg_bytes": "8.25 x evaluated + 14 E_t + 8 |S| + 8 x C3 link vertices",
+                    "evaluated": [e for _, e, _, _ in rows],
+                    "GBps": fr,
                     "GBps_median_pass": statistics.median(fr), "GBps_full_run": tot,
-                    "frac_of_8TBs_median_pass": statistics.median(fr) / 8000.0,
                     "frac_of_measured_median_pass": statistics.median(fr) / pk_meas,
+                    "frac_of_measured_dense_passes": (statistics.median(dense) / pk_meas) if dense else None,
+                    "frac_of_measured_full_run": tot / pk_meas,
                     "frac_of_8TBs_full_run": tot / 8000.0,
-                    "passes_at_40pct_of_8TBs": sum(1 for x in fr if x >= 3200.0),
-                    "note": "change tracking re-evaluates only St(edited) u fired vertices, so "
-                            "late passes exceed the dense-pass bytes/time; dense passes are "
-                            "issue-bound (roofline.ncu)"}
+                    "passes_at_40pct_of_measured": sum(1 for x in fr if x >= 0.4 * pk_meas),
+                    "max_frac_of_measured": max(fr) / pk_meas}
 
     if rank == 0:
         line = {
@@ -480,6 +556,8 @@ def main():
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wname, "V": V, "xi": xi,
+                       "sha256_f": shas["f"], "sha256_ghat": shas["ghat"],
+                       "inputs": "generated on the host CPU (one torch thread), copied to HBM",
                        "iterations": iters, "status": r.status,
                        "ms_setup": r.ms_setup, "ms_loop": r.ms_loop,
                        "l2": f"inputs {4 * V / 1e6:.0f} MB per field > 126 MB L2 (no flush)",
@@ -490,6 +568,7 @@ def main():
             "hbm_frac": roofline["frac"],
             "per_pass": per_pass,
             "roofline": roofline,
+            "roofline_events": roofline_events,
             "cpu_baseline": cpu,
             "e2e": {"value": 4.0 * V / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * V, "d2h_bytes_per_step": 4 * V,

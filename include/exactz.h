@@ -91,7 +91,11 @@ typedef struct {
                           changes, R4 flipped adjacent saddles, R5 join events
                           (R7 flipped adjacent critical points when REFORMULATED),
                           R6 split events */
-  uint64_t walk_steps; /* reserved for diagnostics (0 in this build) */
+  uint64_t walk_steps; /* diagnostics: steps of the C3 label walks (0 when not counted) */
+  uint64_t evaluated;  /* vertices the stencil evaluated this pass (V for a dense pass, the
+                          active set of a change-tracked one; SURVEY 8(d) per-pass bytes) */
+  uint64_t links;      /* link vertices the C3 walks started from this pass (join: |L_g(s)|,
+                          split: |U_g(s)|, summed over the saddles walked) */
   double ms;           /* GPU span of the pass on `stream` (CUDA events; exactz_correct
                           only, 0 elsewhere): detection, edits and the counter read */
 } exactz_iter_stats;

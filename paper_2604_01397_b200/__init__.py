@@ -27,7 +27,8 @@ if not os.path.exists(LIB_PATH):
 
 class IterStats(C.Structure):
     _fields_ = [("violations", C.c_uint64), ("applied", C.c_uint64), ("n", C.c_uint64 * 6),
-                ("walk_steps", C.c_uint64), ("ms", C.c_double)]
+                ("walk_steps", C.c_uint64), ("evaluated", C.c_uint64), ("links", C.c_uint64),
+                ("ms", C.c_double)]
 
 
 class Stats(C.Structure):
@@ -160,6 +161,8 @@ def _result(status, iters, st, rows):
     res = CorrectResult(status, iters.value, table, st.ms_setup, st.ms_loop, kern)
     res.walk_steps = walks
     res.pass_ms = [float(r.ms) for r in rows[:n]] if st.cap else []
+    res.pass_evaluated = [int(r.evaluated) for r in rows[:n]] if st.cap else []
+    res.pass_links = [int(r.links) for r in rows[:n]] if st.cap else []
     res.n_saddles, res.n_join, res.n_split = int(st.n_saddles), int(st.n_join), int(st.n_split)
     return res
 

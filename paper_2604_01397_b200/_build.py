@@ -11,7 +11,7 @@ LIB = os.path.join(PKG, "libexactz.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["exactz.cu"]
-HEADERS = ["kernels.cuh", "mesh.cuh", "sharded.cuh", "stencil_fast.cuh", "vulnerability.cuh", "editlog.cuh"]
+HEADERS = ["kernels.cuh", "mesh.cuh", "sharded.cuh", "stencil_fast.cuh", "stencil_key.cuh", "vulnerability.cuh", "editlog.cuh"]
 
 FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",

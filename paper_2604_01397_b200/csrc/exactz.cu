@@ -4,6 +4,8 @@
 //   if no violation: stop; ApplyBoundedEdits (O9) }.
 // All scratch lives in device memory allocated on the caller's stream; the
 // host reads back 16 counters per round (termination, stats).
+#include <cuda.h>  // CUtensorMap (TMA descriptors; the driver entry point is fetched at run time)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -25,6 +27,7 @@
 #include "../../include/exactz.h"
 #include "kernels.cuh"
 #include "stencil_fast.cuh"
+#include "stencil_key.cuh"
 #include "vulnerability.cuh"
 #include "editlog.cuh"
 
@@ -122,8 +125,23 @@ struct Prof {
   }
 };
 
+// Per-thread, per-device resources a call needs but should not create each
+// time (cudaHostAlloc, stream and event creation cost milliseconds per call
+// in the timed steps): the mapped counter mirror, the two side streams and
+// their fork/join events.  A Ctx borrows the kit when it is free (one call
+// at a time per thread) and otherwise makes its own.
+struct Kit {
+  int dev = -1;
+  bool busy = false;
+  unsigned long long *hcnt = nullptr;
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t fj[3] = {nullptr, nullptr, nullptr};
+};
+static thread_local Kit g_kit;
+
 struct Ctx {
   cudaStream_t s;
+  bool kit = false;  // borrowing g_kit
   Prof prof;
   // Launch one kernel (or library call) of class `cls`; `ours` counts it as
   // one of this library's kernels.
@@ -153,12 +171,61 @@ struct Ctx {
   dim3 rgrid, vblock;                 // persistent row-parallel grid, 128 x-threads
   int zc = 1;
   bool fast = false;                  // every lo >= 0: k_stencil_fast (set by validation)
+  bool keyed = false;                 // value range fits exact SoS keys: k_stencil_key
+  // TMA descriptor of the field the dense stencil reads (k_stencil_key2):
+  // 3D {nx, ny, nz} float32, box {40, 18, 1} from x0 - 4 (the 34 x 18 halo
+  // tile, 16-byte aligned in x), zero fill outside the domain
+  CUtensorMap tmap{};
+  const void *tmap_ptr = nullptr;
+  bool plane_map(const void *g) {
+    if (g == tmap_ptr) return true;
+    if (G.nx % 4 != 0 || ((uintptr_t)g & 15) || G.zoff != 0) return false;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      void *fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+              cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }();
+    if (!encode) return false;
+    const cuuint64_t dim[3] = {(cuuint64_t)G.nx, (cuuint64_t)G.ny, (cuuint64_t)G.nz};
+    const cuuint64_t stride[2] = {(cuuint64_t)G.nx * 4, (cuuint64_t)G.nx * G.ny * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)K2Stage<true>::SXS, (cuuint32_t)K2SY, 1},
+                     estr[3] = {1, 1, 1};
+    if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(g), dim, stride, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    tmap_ptr = g;
+    return true;
+  }
   unsigned long long *cnt = nullptr;  // device counters
   unsigned long long *hcnt = nullptr; // pinned, mapped host mirror
   unsigned long long *hcnt_dev = nullptr;  // its device alias
   Arena arena;
-  explicit Ctx(cudaStream_t st) : s(st), arena(st) {}
+  explicit Ctx(cudaStream_t st) : s(st), arena(st) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    if (!g_kit.busy) {
+      if (g_kit.dev != dev) g_kit = Kit{};  // another device's handles are left to the driver
+      g_kit.dev = dev;
+      g_kit.busy = true;
+      kit = true;
+      hcnt = g_kit.hcnt;
+      for (int k = 0; k < 2; ++k) side[k] = g_kit.side[k];
+      for (int k = 0; k < 3; ++k) fj[k] = g_kit.fj[k];
+    }
+  }
   ~Ctx() {
+    if (kit) {  // hand the (possibly just created) handles back
+      g_kit.hcnt = hcnt;
+      for (int k = 0; k < 2; ++k) g_kit.side[k] = side[k];
+      for (int k = 0; k < 3; ++k) g_kit.fj[k] = fj[k];
+      g_kit.busy = false;
+      return;
+    }
     if (hcnt) cudaFreeHost(hcnt);
     for (int k = 0; k < 2; ++k)
       if (side[k]) cudaStreamDestroy(side[k]);
@@ -235,7 +302,9 @@ struct Ctx {
     // mapped: the fold kernel writes the counters straight into host memory,
     // so a pass's read needs no copy-engine transfer (a bulk D2H of the
     // result on a side stream would otherwise queue every pass behind it)
-    CK(cudaHostAlloc((void **)&hcnt, C_NCOUNTERS * sizeof(unsigned long long), cudaHostAllocMapped));
+    if (!hcnt)
+      CK(cudaHostAlloc((void **)&hcnt, C_NCOUNTERS * sizeof(unsigned long long),
+                       cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void **)&hcnt_dev, hcnt, 0));
     upload_lut();
   }
@@ -258,6 +327,14 @@ struct Ctx {
       ready = true;
     }
     CK(cudaMemcpyToSymbolAsync(d_comp, lut, sizeof(lut), 0, cudaMemcpyHostToDevice, s));
+    static thread_local uint8_t lut2[1 << kSlots];
+    static thread_local bool ready2 = false;
+    if (!ready2) {
+      for (uint32_t m = 0; m < (1u << kSlots); ++m)
+        lut2[m] = (uint8_t)(lut[m] | (lut[~m & ((1u << kSlots) - 1)] << 3));
+      ready2 = true;
+    }
+    CK(cudaMemcpyToSymbolAsync(d_comp2, lut2, sizeof(lut2), 0, cudaMemcpyHostToDevice, s));
   }
   size_t mark_words() const { return (size_t)G.ny * G.nz * G.W; }
   void zero() { CK(cudaMemsetAsync(cnt, 0, C_NALLOC * sizeof(unsigned long long), s)); }
@@ -339,11 +416,12 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
                           int *ntodo = nullptr) {
   if (n <= 0) return;
   const int64_t threads = n;  // one lane per saddle
-  // algorithmic bytes: per saddle its id, its value, 14 link values, the
-  // reached extrema's values and ids
+  // algorithmic bytes: 8 per saddle (id, m1 / M1) here, 8 per
+  // link vertex walked from (its label and the label's value) added after
+  // the pass from the C_LINKS count
   const int cls = FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS;
   if (!ec.rnd) {
-    C.run(cls, 128ull * n, true, [&] {
+    C.run(cls, 8ull * n, true, [&] {
       k_events<SPLIT, FROM_REF, false><<<(unsigned)((threads + 255) / 256), 256, 0, C.s>>>(
           h, sl, n, slots, lm, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt);
     });
@@ -436,7 +514,7 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
 }
 
 struct PassOut {
-  unsigned long long vt, applied, n[6], walk;
+  unsigned long long vt, applied, n[6], walk, evaluated, links;
 };
 
 // One CheckConstraints pass on g (O8) followed by the count and, when
@@ -572,8 +650,32 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
                                                         C.G, C.zc, T, C.cnt);
     });
   } else if (!sparse) {
-    C.run(EXACTZ_K_STENCIL, (uint64_t)C.V * 73 / 8, true, [&] {
-      if (C.fast && trk)
+    // algorithmic bytes: g 4 + packed ref 4 read, mark bit 1/8
+    // written and read: 8.25 B per vertex
+    C.run(EXACTZ_K_STENCIL, (uint64_t)C.V * 33 / 4, true, [&] {
+      // (debug flag 0x4000: the one-row key stencil)
+      const dim3 g2(C.sgrid.x, (unsigned)((C.G.ny + K2TY - 1) / K2TY), C.sgrid.z);
+      // (debug flag 0x8000: thread-staged planes instead of TMA)
+      const bool tma = !(flags & 0x8000u) && C.plane_map(g);
+      if (C.keyed && !(flags & 0x4000u) && trk && tma)
+        k_stencil_key2<true, true><<<g2, TX * K2W, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G, C.zc,
+                                                             T, C.cnt, C.tmap);
+      else if (C.keyed && !(flags & 0x4000u) && tma)
+        k_stencil_key2<false, true><<<g2, TX * K2W, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G,
+                                                              C.zc, T, C.cnt, C.tmap);
+      else if (C.keyed && !(flags & 0x4000u) && trk)
+        k_stencil_key2<true, false><<<g2, TX * K2W, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G,
+                                                              C.zc, T, C.cnt, C.tmap);
+      else if (C.keyed && !(flags & 0x4000u))
+        k_stencil_key2<false, false><<<g2, TX * K2W, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G,
+                                                               C.zc, T, C.cnt, C.tmap);
+      else if (C.keyed && trk)
+        k_stencil_key<true><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G, C.zc,
+                                                           T, C.cnt);
+      else if (C.keyed)
+        k_stencil_key<false><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G, C.zc,
+                                                            T, C.cnt);
+      else if (C.fast && trk)
         k_stencil_fast<true><<<C.sgrid, C.sblock, 0, C.s>>>(g, R.ref, marks, slots, lm, C.G, C.zc,
                                                             T, C.cnt);
       else if (C.fast && (flags & 0x1000u))  // experiment: ALU-pipe lower mask
@@ -653,6 +755,11 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
   C.prof.bytes[EXACTZ_K_EDIT] += 14ull * o.applied;  // f, g, c read; g, c written
   for (int k = 0; k < 6; ++k) o.n[k] = C.hcnt[C_N1 + k];
   o.walk = C.hcnt[C_WALK];
+  // vertices the stencil evaluated: all of them in a dense pass, the list
+  // otherwise (counted by the list / compacted stencils)
+  o.evaluated = (sparse || compact) ? C.hcnt[C_EVAL] : (unsigned long long)C.V;
+  o.links = C.hcnt[C_LINKS];
+  C.prof.bytes[EXACTZ_K_EVENTS] += 8ull * o.links;
   return o;
 }
 
@@ -664,6 +771,15 @@ static void validate_inputs(Ctx &C, const float *f, const float *g, float xi,
   C.read();
   // debug flag 0x800: the general stencil even for non-negative fields
   C.fast = C.hcnt[C_NEG] == 0 && !(flags & 0x800u);
+  // exact SoS keys (stencil_key.cuh) when every value g takes, [lo_min,
+  // ghat_max], is within [2^-41, 2^63) and spans < 2^28 bit patterns
+  // (debug flag 0x2000: off)
+  {
+    const uint32_t lo_min = ~(uint32_t)C.hcnt[C_KEYMIN], g_max = (uint32_t)C.hcnt[C_KEYMAX];
+    C.keyed = C.fast && !(flags & 0x2000u) && lo_min >= kKeyLoMinBits && g_max < kKeyHiMaxBits &&
+              g_max >= lo_min && g_max - lo_min < kKeySpan;
+    for (int s = 0; s < kSlots; ++s) C.G.kc[s] = (uint32_t)s - 16u * lo_min;
+  }
   if (C.hcnt[C_BAD_NF]) {
     set_err("validate", "non-finite value in f or g");
     throw Error{EXACTZ_EINVAL};
@@ -673,6 +789,31 @@ static void validate_inputs(Ctx &C, const float *f, const float *g, float xi,
     throw Error{EXACTZ_EBOUND};
   }
 }
+
+// Timing events of the per-pass stats rows, kept across calls (per thread and
+// device): creating two events per pass cost the timed bench steps ~4 ms.
+struct EventPool {
+  int dev = -1;
+  std::vector<cudaEvent_t> free;
+};
+static thread_local EventPool g_evpool;
+static cudaEvent_t pass_event() {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev != g_evpool.dev) {
+    g_evpool.free.clear();  // events of another device are left to the driver
+    g_evpool.dev = dev;
+  }
+  if (!g_evpool.free.empty()) {
+    cudaEvent_t e = g_evpool.free.back();
+    g_evpool.free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+static void pass_event_put(cudaEvent_t e) { g_evpool.free.push_back(e); }
 
 // g_ready (exactz_correct_host): an event recorded after g_in's host->device
 // copy, which may still be running when the call starts; the reference of f
@@ -812,8 +953,8 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     // per-pass GPU span for the stats rows (events read after the final sync)
     cudaEvent_t pa = nullptr, pb = nullptr;
     if (stats && stats->rows && rows < stats->cap) {
-      CK(cudaEventCreate(&pa));
-      CK(cudaEventCreate(&pb));
+      pa = pass_event();
+      pb = pass_event();
       CK(cudaEventRecord(pa, s));
     }
     PassOut o = detect_and_edit(C, R, f, out, c, marks, slots, lm, eps, delta, N, flags, may_edit,
@@ -840,6 +981,8 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       r.applied = o.applied;
       for (int k = 0; k < 6; ++k) r.n[k] = o.n[k];
       r.walk_steps = o.walk;
+      r.evaluated = o.evaluated;
+      r.links = o.links;
       r.ms = 0.0;  // set from the pass events after the final sync
     }
     ++rows;
@@ -910,8 +1053,8 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     }
   }
   for (auto &e : pass_ev) {
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
+    pass_event_put(e.first);
+    pass_event_put(e.second);
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -1038,6 +1181,8 @@ exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3]
       row->applied = 0;
       for (int k = 0; k < 6; ++k) row->n[k] = o.n[k];
       row->walk_steps = o.walk;
+      row->evaluated = o.evaluated;
+      row->links = o.links;
       row->ms = 0.0;
     }
     CK(cudaStreamSynchronize(s));

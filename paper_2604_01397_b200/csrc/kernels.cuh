@@ -46,7 +46,9 @@ enum Counter {
   C_WALK = 15,     // diagnostic: steps taken by the label walks of a pass
   C_NCP = 8,       // reference: critical points (shares the slot of C_CHANGED)
   C_NEG = 16,      // validation: lo = RU(f - xi) < 0 or g = -0.0 (k_stencil_fast needs none)
-  C_NCOUNTERS = 18
+  C_EVAL = 17,     // diagnostic: vertices evaluated by the list / compacted stencils of a pass
+  C_LINKS = 18,    // diagnostic: link vertices the C3 walks started from in a pass
+  C_NCOUNTERS = 19
 };
 
 // Geometry of the (local) grid a kernel works on.  Single GPU: the whole
@@ -66,6 +68,8 @@ struct GridP {
   // immediates ptxas emits two)
   uint32_t keymask;   // ~15u
   uint32_t tag[16];   // tag[k] = k
+  // k_stencil_key: key of slot s = bits * 16 + kc[s], kc[s] = s - 16 bits(lo_min)
+  uint32_t kc[kSlots];
 };
 
 // Magic numbers of the unsigned division n / d for n < 2^31, d >= 1
@@ -344,6 +348,7 @@ __device__ __forceinline__ bool sos_less_g(const float *h, int u, int v) {
 __global__ void k_validate(const float *__restrict__ f, const float *__restrict__ g, int64_t V,
                            float xi, unsigned long long *cnt) {
   unsigned nf = 0, nb = 0, ng = 0;
+  uint32_t nlo = 0, ghi = 0;  // ~bits of the smallest lo, bits of the largest g (lo, g >= 0)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V;
        i += (int64_t)gridDim.x * blockDim.x) {
     float a = f[i], b = g[i];
@@ -354,10 +359,20 @@ __global__ void k_validate(const float *__restrict__ f, const float *__restrict_
     float lo = __fsub_ru(a, xi), hi = __fadd_rd(a, xi);
     if (!(lo <= b && b <= hi)) ++nb;
     if (lo < 0.0f || __float_as_uint(b) == 0x80000000u) ++ng;  // -0.0 in g: general stencil
+    nlo = max(nlo, ~__float_as_uint(lo));
+    ghi = max(ghi, __float_as_uint(b));
   }
   warp_add(&cnt[C_BAD_NF], nf);
   warp_add(&cnt[C_BAD_BOUND], nb);
   warp_add(&cnt[C_NEG], ng);
+  // value range of g over the call (k_stencil_key's applicability); only
+  // read when C_NEG == 0, where bit order == value order
+  nlo = __reduce_max_sync(0xffffffffu, nlo);
+  ghi = __reduce_max_sync(0xffffffffu, ghi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&cnt[C_KEYMIN], (unsigned long long)nlo);
+    atomicMax(&cnt[C_KEYMAX], (unsigned long long)ghi);
+  }
 }
 
 // ------------------------------------------------------ reference of f (O7)
@@ -811,6 +826,7 @@ __global__ void __launch_bounds__(NT, 5) k_stencil_compact(const float *__restri
   const uint32_t xin = (G.nx - x0 >= 32) ? 0xffffffffu : ((1u << (G.nx - x0)) - 1u);
   unsigned n1 = 0, n2 = 0, n3 = 0;
   const PlaneCells pc = plane_cells(x0, y0, G);
+  unsigned ne = 0;  // vertices evaluated (C_EVAL)
 
   // active lanes of this warp's row in plane p -> list[p & 3]
   auto build = [&](int p) {
@@ -862,6 +878,7 @@ __global__ void __launch_bounds__(NT, 5) k_stencil_compact(const float *__restri
 
     bool schg = false;
     if (tid < ln[z & 3]) {
+      ++ne;
       const int cell = list[z & 3][tid];
       const int lx = cell & 31, ly = cell >> 5;
       const int x = x0 + lx, y = y0 + ly;
@@ -942,6 +959,7 @@ __global__ void __launch_bounds__(NT, 5) k_stencil_compact(const float *__restri
   warp_add(&cnt[C_N1 + 0], n1);
   warp_add(&cnt[C_N1 + 1], n2);
   warp_add(&cnt[C_N1 + 2], n3);
+  warp_add(&cnt[C_EVAL], ne);
 }
 
 // Sparse pass (tracking): re-evaluate only the active vertices (warp per
@@ -1165,9 +1183,12 @@ __global__ void __launch_bounds__(256) k_stencil_list(const float *__restrict__ 
                                                       const int *__restrict__ count, GridP G,
                                                       Track T, unsigned long long *cnt) {
   const int n = *count;
-  unsigned n1 = 0, n2 = 0, n3 = 0;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+  unsigned n1 = 0, n2 = 0, n3 = 0, ne = 0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     vertex_pass(__ldg(&list[k]), g, ref, marks, slots, lm, G, T, n1, n2, n3);
+    ++ne;
+  }
+  warp_add(&cnt[C_EVAL], ne);
   warp_add(&cnt[C_N1 + 0], n1);
   warp_add(&cnt[C_N1 + 1], n2);
   warp_add(&cnt[C_N1 + 2], n3);
@@ -1410,6 +1431,7 @@ __device__ __forceinline__ unsigned events_group(
                 uz = sz + sg1 * (bb >> 2);
       if (CACHE) brick_bit(ux, uy, uz, bsx, bsy, bsz, mask);
       if (lower != SPLIT) {
+        if (!FROM_REF) atomicAdd(&cnt[(size_t)(1 + (blockIdx.x & (kCntRep - 1))) * kCntStride + C_LINKS], 1ull);
         int e;
         if constexpr (CACHE) e = walk_track<SPLIT>(u, ux, uy, uz, slots, G, bsx, bsy, bsz, mask);
         else e = walk<SPLIT, FROM_REF, SLAB>(u, slots, ref, G);
@@ -1491,7 +1513,7 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
   __syncthreads();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int A = G.nx * G.ny, off = G.zoff * A, lo = G.zb * A, hi = G.ze * A;
-  unsigned hit = 0;
+  unsigned hit = 0, links = 0;
   if (k < n) {
     const int s = __ldg(&sl[k]) - off;  // local
     uint32_t todo;                       // link slots to walk from
@@ -1510,6 +1532,7 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
     } else {
       const uint32_t m = __ldg(&lm[s]);
       todo = SPLIT ? (m >> 16) : (m & 0xFFFFu);
+      links = __popc(todo);
     }
     int best = -1;
     float bv = 0.0f;
@@ -1582,7 +1605,10 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
       }
     }
   }
-  if (!FROM_REF) warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
+  if (!FROM_REF) {
+    warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
+    warp_add(&cnt[C_LINKS], links);
+  }
 }
 
 // Tracking: a saddle whose cached result is still valid (no brick it depends
@@ -1693,7 +1719,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
   }
   __syncthreads();
   const int n = *ntodo;
-  unsigned hit = 0;
+  unsigned hit = 0, links = 0;
   if (n * 16 <= (int)(gridDim.x * blockDim.x)) {
     // few saddles (late passes: mostly long walks that never stay cached):
     // 16 lanes per saddle, one walk per lane, for the shortest critical path
@@ -1719,6 +1745,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
       brick_bit(sx + (p & 3) - 1, sy + ((p >> 2) & 3) - 1, sz + (p >> 4) - 1, bsx, bsy, bsz, mask);
     }
     uint32_t rest = SPLIT ? (m >> 16) : (m & 0xFFFFu);
+    links += __popc(rest);
     int best = -1;
     float bv = 0.0f;
     int w[2] = {0, 0}, x[2] = {0, 0}, y[2] = {0, 0}, z[2] = {0, 0};
@@ -1776,6 +1803,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
     }
   }
   warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
+  warp_add(&cnt[C_LINKS], links);
 }
 
 // ------------------------------------------------ sharded helpers (z-slabs)

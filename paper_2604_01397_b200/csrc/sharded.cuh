@@ -771,6 +771,8 @@ static exactz_status sharded_impl(Transport &T, std::vector<const float *> f_in,
       r.applied = o[C_APPLIED];
       for (int k = 0; k < 6; ++k) r.n[k] = o[C_N1 + k];
       r.walk_steps = 0;
+      r.evaluated = 0;
+      r.links = 0;
       r.ms = 0.0;  // per-pass spans: single-GPU call only
     }
     ++rows;
