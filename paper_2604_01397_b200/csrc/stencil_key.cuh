@@ -383,11 +383,13 @@ __device__ __forceinline__ KeyOut key_rules(const uint32_t (&bv)[kSlots], uint32
   KeyOut o;
   o.lower = (__float_as_uint(acc) - 0x4B000000u) & valid;
   o.upper = valid & ~o.lower;
-  const int up = o.upper ? (int)(kmax & 15u) : kSelf;
-  const int dn = o.lower ? (int)(kmin & 15u) : kSelf;
+  const uint32_t up = o.upper ? (kmax & 15u) : (uint32_t)kSelf;
+  const uint32_t dn = o.lower ? (kmin & 15u) : (uint32_t)kSelf;
+  // R1 / R2: the packed slot byte against f's (ref bits 14..21 = dn_f | up_f << 4)
+  const uint32_t ns = dn | (up << 4), rf = (r >> 14) & 0xFFu, d = ns ^ rf;
   uint32_t tgt = 0;
-  if (up != ref_up(r)) { tgt |= 1u << up; n1 += 1; }
-  if (dn != ref_dn(r)) { tgt |= 1u << ref_dn(r); n2 += 1; }
+  if (d & 0xF0u) { tgt |= 1u << up; n1 += 1; }
+  if (d & 0x0Fu) { tgt |= 1u << (rf & 15u); n2 += 1; }
   // R3, branch-free (in the dense passes nearly every vertex has a flipped
   // pair): the type from the interior LUT, re-read for the rare face vertex
   const uint32_t flow = ref_flow(r);
@@ -400,7 +402,7 @@ __device__ __forceinline__ KeyOut key_rules(const uint32_t (&bv)[kSlots], uint32
   n3 += __popc(fl);
   tgt |= (fl & flow) | ((fl & ~flow) ? (1u << kSelf) : 0u);
   o.tgt = tgt;
-  o.ns = (uint8_t)(dn | (up << 4));
+  o.ns = (uint8_t)ns;
   return o;
 }
 
@@ -504,7 +506,10 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
   const bool ina = x < G.nx && ya < G.ny, inb = x < G.nx && yb < G.ny;
   const int ca = (2 * w + 1) * SXS + tx + K2Stage<TMA>::X0;  // row a's cell; row b's: + SXS
   const uint32_t vxya = valid_xy(x, ya, G), vxyb = valid_xy(x, yb, G);
-  const uint32_t ptx = 1u << tx;
+  // 2^tx, opaque to the compiler: the row placement cb * 2^tx stays an IMAD
+  // (FMA pipe) instead of becoming a shift on the busier ALU pipe
+  uint32_t ptx = 1u << tx;
+  asm volatile("mov.b32 %0, %0;" : "+r"(ptx));
   unsigned n1 = 0, n2 = 0, n3 = 0;
   const int A = G.nx * G.ny;
   auto slot_of = [&](int p) { return (p - z0 + 1) & 3; };  // ring slot of plane p
@@ -594,6 +599,9 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
   fetch_pos(0, q0);
   fetch_pos(1, q1);
   int flushed = z0 - 2;  // planes <= flushed are in the global bitmap
+  // output pointers of row a in plane z (row b: + nx), advanced per step
+  uint8_t *slp = slots + ia0;
+  uint32_t *lmp = lm + ia0;
 
   auto step = [&](int z, Pre &cur) {
     const int dz = z - z0;
@@ -602,7 +610,6 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
     if (prefetch) load(gpl, z + 2 < G.nz, pre);
     gpl += A;
     if (TMA) wait_plane(z + 1);
-    const int ia = ia0 + dz * A, ib = ia + G.nx;
     const uint32_t vz = valid_z(z, G);
     const uint32_t va = vxya & vz, vb = vxyb & vz;
     const bool edge = __any_sync(0xffffffffu, (va & vb) != 0x3FFFu);
@@ -641,21 +648,23 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
     n1 += m1; n2 += m2; n3 += m3;
     bool schg = false;
     if (ina) {
-      if (TRACK && T.bval) schg = slots[ia] != oa.ns;
-      slots[ia] = oa.ns;
+      if (TRACK && T.bval) schg = *slp != oa.ns;
+      *slp = oa.ns;
       if (ref_saddle(cur.ra)) {
-        lm[ia] = oa.lower | (oa.upper << 16);
+        *lmp = oa.lower | (oa.upper << 16);
         if (T.gS) T.gS[cur.pa] = c00;
       }
     }
     if (inb) {
-      if (TRACK && T.bval) schg |= slots[ib] != ob.ns;
-      slots[ib] = ob.ns;
+      if (TRACK && T.bval) schg |= slp[G.nx] != ob.ns;
+      slp[G.nx] = ob.ns;
       if (ref_saddle(cur.rb)) {
-        lm[ib] = ob.lower | (ob.upper << 16);
+        lmp[G.nx] = ob.lower | (ob.upper << 16);
         if (T.gS) T.gS[cur.pb] = c01;
       }
     }
+    slp += A;
+    lmp += A;
     fetch(dz + 3, cur);
     if (TRACK && T.bval) {
       const unsigned chg = __ballot_sync(0xffffffffu, schg);
