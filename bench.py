@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong = the z-slabs of one config field; weak = one "
+                         "config-sized field per rank stacked along z (P:577-589)")
     ap.add_argument("--impl", default="exactz", choices=["exactz", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ocr", action="store_true", help="skip the SZ-like OCR report")
@@ -280,13 +283,39 @@ def main():
     import paper_2604_01397_b200 as E
     from synth import fields as S
 
-    f, g, xi, shas, golden = make_inputs(args.config)
-    f, g = f.to(dev), g.to(dev)
-    V = f.numel()
+    weak = args.scaling == "weak" and ws > 1
+    if weak:
+        # weak scaling: rank r holds its own config-sized field
+        # (same recipe, seed offset r), the ranks' fields stacked along z form
+        # one (nx, ny, ws * nz) field; one xi for all (the smallest rank's
+        # rel * range, so that min f >= xi holds on every rank)
+        f, g, xi_r = S.make(args.config, device=dev, seed_offset=rank)
+        t = torch.tensor([xi_r], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        xi = float(t.item())
+        f, g, _ = S.make(args.config, device=dev, seed_offset=rank, xi=xi)
+        shas, golden = {"f": None, "ghat": None}, None
+        V = f.numel() * ws
+    else:
+        f, g, xi, shas, golden = make_inputs(args.config)
+        f, g = f.to(dev), g.to(dev)
+        V = f.numel()
     wname = workload_name(args.config, f)
+    if weak:
+        wname += f" per rank, x{ws} stacked along z (weak scaling)"
     stream = torch.cuda.current_stream()
     sharded = ws > 1
-    if sharded:
+    if weak:
+        from paper_2604_01397_b200 import dist as D
+        comm = D.open_comm(local)
+        dims = (f.shape[2], f.shape[1], f.shape[0] * ws)
+        f_run, g_run = f, g
+        out = torch.empty_like(g_run)
+
+        def step(profile=False):
+            return E.exactz_correct_sharded(comm, f_run, g_run, dims, xi, out=out,
+                                            stats_cap=1024)
+    elif sharded:
         # strong scaling: the z-slabs of ONE field over the ranks (NCCL inside)
         from paper_2604_01397_b200 import dist as D
         comm = D.open_comm(local)
@@ -553,7 +582,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "higher_is_better": True, "scaling": "strong" if sharded and not weak else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wname, "V": V, "xi": xi,
                        "sha256_f": shas["f"], "sha256_ghat": shas["ghat"],

@@ -136,6 +136,7 @@ struct Kit {
   unsigned long long *hcnt = nullptr;
   cudaStream_t side[2] = {nullptr, nullptr};
   cudaEvent_t fj[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fev[2] = {nullptr, nullptr};
 };
 static thread_local Kit g_kit;
 
@@ -216,6 +217,7 @@ struct Ctx {
       hcnt = g_kit.hcnt;
       for (int k = 0; k < 2; ++k) side[k] = g_kit.side[k];
       for (int k = 0; k < 3; ++k) fj[k] = g_kit.fj[k];
+      for (int k = 0; k < 2; ++k) fev[k] = g_kit.fev[k];
     }
   }
   ~Ctx() {
@@ -223,6 +225,7 @@ struct Ctx {
       g_kit.hcnt = hcnt;
       for (int k = 0; k < 2; ++k) g_kit.side[k] = side[k];
       for (int k = 0; k < 3; ++k) g_kit.fj[k] = fj[k];
+      for (int k = 0; k < 2; ++k) g_kit.fev[k] = fev[k];
       g_kit.busy = false;
       return;
     }
@@ -231,10 +234,13 @@ struct Ctx {
       if (side[k]) cudaStreamDestroy(side[k]);
     for (int k = 0; k < 3; ++k)
       if (fj[k]) cudaEventDestroy(fj[k]);
+    for (int k = 0; k < 2; ++k)
+      if (fev[k]) cudaEventDestroy(fev[k]);
   }
   // fork/join of two side streams (independent kernels of one pass)
   cudaStream_t side[2] = {nullptr, nullptr};
   cudaEvent_t fj[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fev[2] = {nullptr, nullptr};  // fold of counter buffer 0 / 1 done
   cudaStream_t main_s = nullptr;
   void fork() {
     if (!side[0]) {
@@ -302,8 +308,9 @@ struct Ctx {
     // mapped: the fold kernel writes the counters straight into host memory,
     // so a pass's read needs no copy-engine transfer (a bulk D2H of the
     // result on a side stream would otherwise queue every pass behind it)
+    // two buffers: a pass's counters are read while the next pass runs
     if (!hcnt)
-      CK(cudaHostAlloc((void **)&hcnt, C_NCOUNTERS * sizeof(unsigned long long),
+      CK(cudaHostAlloc((void **)&hcnt, 2 * C_NCOUNTERS * sizeof(unsigned long long),
                        cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void **)&hcnt_dev, hcnt, 0));
     upload_lut();
@@ -344,6 +351,20 @@ struct Ctx {
     g_launches++;
     CK(cudaStreamSynchronize(s));
     if (prof.on) prof.drain();
+  }
+  // Asynchronous counter read of a pass: fold into mapped buffer `buf` and
+  // record its event; counters(buf) waits for that event only, so the host can
+  // enqueue the next pass before this one has finished.
+  void fold(int buf) {
+    if (!fev[buf]) CK(cudaEventCreateWithFlags(&fev[buf], cudaEventDisableTiming));
+    k_fold_counters<<<1, 32, 0, s>>>(cnt, hcnt_dev + (size_t)buf * C_NCOUNTERS);
+    g_launches++;
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(fev[buf], s));
+  }
+  const unsigned long long *counters(int buf) {
+    CK(cudaEventSynchronize(fev[buf]));
+    return hcnt + (size_t)buf * C_NCOUNTERS;
   }
 };
 
@@ -409,29 +430,70 @@ static void sort_ids(Ctx &C, uint64_t *keys, int n, int32_t *ids) {
   });
 }
 
+// k_fclean over all n saddles (one per thread) or over an idx list (a small
+// grid-stride grid: the list is short in late passes)
+template <bool SPLIT>
+static void launch_fclean(Ctx &C, const float *h, const int32_t *sl, int n, const uint32_t *lm,
+                          const uint32_t *ref, const FPaths &fp, const int32_t *ext,
+                          uint32_t *marks, int *out, int *nout, const int *idx, const int *nidx,
+                          EvCache ec, int round) {
+  const unsigned grid = idx ? 148u * 4u : (unsigned)((n + 255) / 256);
+  k_fclean<SPLIT><<<grid, 256, 0, C.s>>>(h, sl, n, lm, ref, fp, ext, marks, C.G, out, nout,
+                                         C.cnt, idx, nidx, ec, round);
+}
+
+// The C3 walks of one saddle list.  fp.off (tracking, list passes): the
+// clean-path test first (k_fclean), only the saddles it leaves (ftodo) go on;
+// ec.rnd: the brick-stamp cache (k_events_check), then the walks of what is
+// left (k_events_cached); else every saddle is walked (k_events).
 template <bool SPLIT, bool FROM_REF>
 static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, const uint8_t *slots,
                           const uint32_t *lm, const uint32_t *ref, int32_t *ext, uint32_t *marks,
                           EvCache ec = EvCache{}, Track tr = Track{}, int *todo = nullptr,
-                          int *ntodo = nullptr) {
+                          int *ntodo = nullptr, FPaths fp = FPaths{}, int *ftodo = nullptr,
+                          int *nftodo = nullptr) {
   if (n <= 0) return;
   const int64_t threads = n;  // one lane per saddle
   // algorithmic bytes: 8 per saddle (id, m1 / M1) here, 8 per
   // link vertex walked from (its label and the label's value) added after
   // the pass from the C_LINKS count
   const int cls = FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS;
+  const int *idx = nullptr, *nidx = nullptr;
+  if (!FROM_REF && fp.off && !ec.rnd) {
+    CK(cudaMemsetAsync(nftodo, 0, sizeof(int), C.s));
+    // bytes: id, lm, ref word, offsets (16 B per saddle); the tile entries
+    // and their flags are not counted (test overhead)
+    C.run(cls, 16ull * n, true, [&] {
+      launch_fclean<SPLIT>(C, h, sl, n, lm, ref, fp, ext, marks, ftodo, nftodo, nullptr, nullptr,
+                           EvCache{}, 0);
+    });
+    idx = ftodo;
+    nidx = nftodo;
+  }
   if (!ec.rnd) {
+    // (an idx list: a small grid-stride grid)
+    const unsigned grid = idx ? 148u * 8u : (unsigned)((threads + 255) / 256);
     C.run(cls, 8ull * n, true, [&] {
-      k_events<SPLIT, FROM_REF, false><<<(unsigned)((threads + 255) / 256), 256, 0, C.s>>>(
-          h, sl, n, slots, lm, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt);
+      k_events<SPLIT, FROM_REF, false><<<grid, 256, 0, C.s>>>(
+          h, sl, n, slots, lm, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt,
+          idx, nidx);
     });
     return;
   }
   CK(cudaMemsetAsync(ntodo, 0, sizeof(int), C.s));
   C.run(cls, 16ull * n, true, [&] {
-    k_events_check<SPLIT><<<(unsigned)((n + 255) / 256), 256, 0, C.s>>>(sl, n, ec, tr, marks,
-                                                                        C.G, todo, ntodo, C.cnt);
+    k_events_check<SPLIT><<<(unsigned)((n + 255) / 256), 256, 0, C.s>>>(
+        sl, n, ec, tr, marks, C.G, todo, ntodo, C.cnt, idx, nidx);
   });
+  if (fp.off) {  // the clean-path test on what the stamps left (caching the clean ones)
+    CK(cudaMemsetAsync(nftodo, 0, sizeof(int), C.s));
+    C.run(cls, 0, true, [&] {
+      launch_fclean<SPLIT>(C, h, sl, n, lm, ref, fp, ext, marks, ftodo, nftodo, todo, ntodo, ec,
+                           tr.round);
+    });
+    todo = ftodo;
+    ntodo = nftodo;
+  }
   C.run(cls, 0, true, [&] {
     k_events_cached<SPLIT><<<148 * 16, 256, 0, C.s>>>(h, sl, todo, ntodo, slots, lm, ext, marks,
                                                       C.G,
@@ -440,7 +502,8 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
 }
 
 // O7: reference topology of f, computed once per call.
-static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = false) {
+static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = false,
+                            bool ext_by_fpaths = false) {
   int64_t V = C.V;
   R.ref = C.arena.get<uint32_t>(V);
   uint64_t *keys = C.arena.get<uint64_t>(V);
@@ -503,7 +566,7 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
   R.m1 = C.arena.get<int32_t>(R.nJ);
   R.M1 = C.arena.get<int32_t>(R.nP);
   // m1 / M1 by walking f's steepest paths from each saddle's link
-  if (!reform) {  // the two lists concurrently on the side streams
+  if (!reform && !ext_by_fpaths) {  // the two lists concurrently on the side streams
     C.fork();
     C.on_side(0);
     launch_events<false, true>(C, f, R.J, R.nJ, nullptr, nullptr, R.ref, R.m1, nullptr);
@@ -537,6 +600,95 @@ struct Tracking {
   uint16_t *bval = nullptr, *bslot = nullptr, *sbval = nullptr, *sbslot = nullptr;
   EvCache ecJ{}, ecP{};
   int *todo = nullptr, *ntodo = nullptr, *todoP = nullptr;
+  // clean-path test of the C3 walks (kernels.cuh FPaths; list passes only)
+  bool fp_on = false;
+  // per pass and list (join, split): run the test only where it is expected
+  // to pay: P(a saddle is clean) ~ (1 - d)^L >= fp_gate, with d the fraction
+  // of dirty tiles (bounded by the R1 + R2 firings of the last pass read, over
+  // the tile count) and L the average tile entries per saddle
+  bool fp_use[2] = {false, false};
+  double fpL[2] = {0.0, 0.0};
+  unsigned long long last_n12 = ~0ull;
+  void fp_gate(double gate) {
+    const double d = nt ? std::min(1.0, (double)last_n12 / (double)nt) : 1.0;
+    for (int k = 0; k < 2; ++k) fp_use[k] = fp_on && std::pow(1.0 - d, fpL[k]) >= gate;
+  }
+  int ntx = 0, nty = 0, ntz = 0, nt = 0;
+  FPaths fpJ{}, fpP{};
+  uint32_t *dirtD = nullptr, *dirtU = nullptr;  // bitmaps of ntiles bits
+  int *ftodo = nullptr, *ftodoP = nullptr, *nftodo = nullptr;
+  template <bool SPLIT>
+  FPaths fpaths(Ctx &C, const Reference &R, const int32_t *sl, int n, unsigned long long *bump,
+               unsigned long long *diag, const float *f, int32_t *ext) {
+    FPaths F{};
+    const size_t m = n ? (size_t)n : 1;
+    int64_t *off = C.arena.get<int64_t>(m);
+    uint16_t *len = C.arena.get<uint16_t>(m);
+    int32_t *lab = C.arena.get<int32_t>(m * kFLab);
+    uint8_t *nlab = C.arena.get<uint8_t>(m);
+    unsigned long long *bmask = C.arena.get<unsigned long long>(m);
+    // tile entries: 24 per saddle on average (C2 ~9, C3 ~?; a warp that
+    // does not fit leaves its saddles to the walks)
+    const unsigned long long cap = 24ull * m + 4096;
+    int32_t *tiles = C.arena.get<int32_t>(cap);
+    if (n > 0)
+      C.run(EXACTZ_K_REFERENCE, 8ull * n, true, [&] {
+        k_fpaths<SPLIT><<<(unsigned)((n + 255) / 256), 256, 0, C.s>>>(
+            sl, n, R.ref, C.G, ntx, nty, bump, cap, off, len, tiles, lab, nlab, bmask, diag, f,
+            ext);
+      });
+    F.off = off;
+    F.len = len;
+    F.tiles = tiles;
+    F.lab = lab;
+    F.nlab = nlab;
+    F.bmask = bmask;
+    return F;
+  }
+  // at setup, in place of the reference walks of build_reference: also
+  // writes R.m1 / R.M1
+  void start_fpaths(Ctx &C, const Reference &R, const float *f) {
+    ntx = (C.G.nx + (1 << FTX_SH) - 1) >> FTX_SH;
+    nty = (C.G.ny + (1 << FTY_SH) - 1) >> FTY_SH;
+    ntz = (C.G.nz + (1 << FTZ_SH) - 1) >> FTZ_SH;
+    nt = ntx * nty * ntz;
+    const size_t nw = ((size_t)nt + 31) / 32;
+    dirtD = C.arena.get<uint32_t>(2 * nw);
+    dirtU = dirtD + nw;
+    unsigned long long *bump = C.arena.get<unsigned long long>(2);
+    CK(cudaMemsetAsync(bump, 0, 2 * sizeof(unsigned long long), C.s));
+    static const bool tl = std::getenv("EXACTZ_TIMELINE") != nullptr;  // diagnostic
+    unsigned long long *diag = nullptr;
+    if (tl) {
+      diag = C.arena.get<unsigned long long>(8);
+      CK(cudaMemsetAsync(diag, 0, 8 * sizeof(unsigned long long), C.s));
+    }
+    fpJ = fpaths<false>(C, R, R.J, R.nJ, bump, diag, f, R.m1);
+    fpP = fpaths<true>(C, R, R.P, R.nP, bump + 1, diag ? diag + 4 : nullptr, f, R.M1);
+    if (tl) {
+      unsigned long long h[8];
+      CK(cudaMemcpyAsync(h, diag, sizeof(h), cudaMemcpyDeviceToHost, C.s));
+      CK(cudaStreamSynchronize(C.s));
+      std::fprintf(stderr,
+                   "fpaths J %d: long %llu labels %llu full %llu entries %llu | P %d: long %llu "
+                   "labels %llu full %llu entries %llu\n",
+                   R.nJ, h[0], h[1], h[2], h[3], R.nP, h[4], h[5], h[6], h[7]);
+    }
+    fpJ.dirt = dirtD;
+    fpP.dirt = dirtU;
+    fpJ.nt = fpP.nt = nt;
+    {  // average tile entries per saddle (the gate below)
+      unsigned long long h[2];
+      CK(cudaMemcpyAsync(h, bump, sizeof(h), cudaMemcpyDeviceToHost, C.s));
+      CK(cudaStreamSynchronize(C.s));
+      fpL[0] = R.nJ ? (double)h[0] / R.nJ : 0.0;
+      fpL[1] = R.nP ? (double)h[1] / R.nP : 0.0;
+    }
+    ftodo = C.arena.get<int>(R.nJ > 0 ? R.nJ : 1);
+    ftodoP = C.arena.get<int>(R.nP > 0 ? R.nP : 1);
+    nftodo = C.arena.get<int>(2);
+    fp_on = true;
+  }
   void geometry(const Ctx &C) {
     nbx = (C.G.nx + BX - 1) / BX;
     nby = (C.G.ny + BY - 1) / BY;
@@ -624,11 +776,14 @@ struct HostSnap {
 // With tracking: a sparse pass re-evaluates only the active vertices, and
 // cached C3 results are reused while their bricks are unchanged (exact; see
 // kernels.cuh Track).
-static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float *g, uint8_t *c,
+struct PassTicket {
+  int buf = 0;            // counter buffer of the pass (Ctx::fold)
+  bool listed = false;    // the stencil counted the vertices it evaluated (C_EVAL)
+};
+static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float *g, uint8_t *c,
                                uint32_t *marks, uint8_t *slots, uint32_t *lm, float xi,
-                               float delta, int N,
-                               uint32_t flags, bool do_edit, Tracking *trk = nullptr,
-                               int round = 0) {
+                               float delta, int N, uint32_t flags, bool do_edit,
+                               Tracking *trk = nullptr, int round = 0, int buf = 0) {
   bool c3 = !(flags & EXACTZ_NO_C3);
   C.zero();
   Track T = trk ? trk->track(round) : Track{};
@@ -636,6 +791,9 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
   T.gS = R.gS;
   const bool sparse = trk && trk->ready && trk->sparse;
   const bool compact = trk && trk->ready && !trk->sparse;
+  // the clean-path test needs every vertex with a non-f pointer flagged: list
+  // passes only (the list stencil flags; an unlisted vertex has f's pointers)
+  const bool fpass = sparse && trk->fp_on && (trk->fp_use[0] || trk->fp_use[1]);
   // algorithmic bytes per vertex: g 4 + ref 4 read, slots 1 + mark bits 1/8
   // written; a sparse or compacted pass: the active vertices
   // only (plus the activity bitmap)
@@ -693,6 +851,13 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
     });
   } else {
     CK(cudaMemsetAsync(trk->nlist, 0, sizeof(int), C.s));
+    if (fpass) {  // this pass's dirty tiles (vertex_pass)
+      CK(cudaMemsetAsync(trk->dirtD, 0, 2 * (((size_t)trk->nt + 31) / 32) * 4, C.s));
+      T.dirtD = trk->dirtD;
+      T.dirtU = trk->dirtU;
+      T.ntx = trk->ntx;
+      T.nty = trk->nty;
+    }
     C.run(EXACTZ_K_SPARSE, (uint64_t)C.V / 8, true, [&] {
       k_act_list<<<148 * 16, 256, 0, C.s>>>(trk->act[trk->cur],
                                             trk->edited_valid ? trk->edited : nullptr, C.G,
@@ -725,11 +890,15 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
     const bool cache = trk && trk->cache_on;
     launch_events<true, false>(C, g, R.P, R.nP, slots, lm, R.ref, R.M1, marks,
                                cache ? trk->ecP : EvCache{}, T, cache ? trk->todoP : nullptr,
-                               cache ? trk->ntodo + 1 : nullptr);
+                               cache ? trk->ntodo + 1 : nullptr,
+                               fpass && trk->fp_use[1] ? trk->fpP : FPaths{},
+                               fpass ? trk->ftodoP : nullptr, fpass ? trk->nftodo + 1 : nullptr);
     C.on_side(0);
     launch_events<false, false>(C, g, R.J, R.nJ, slots, lm, R.ref, R.m1, marks,
                                 cache ? trk->ecJ : EvCache{}, T, cache ? trk->todo : nullptr,
-                                cache ? trk->ntodo : nullptr);
+                                cache ? trk->ntodo : nullptr,
+                                fpass && trk->fp_use[0] ? trk->fpJ : FPaths{},
+                                fpass ? trk->ftodo : nullptr, fpass ? trk->nftodo : nullptr);
   }
   C.join();
   if (trk && trk->act_on && trk->pull_stars)  // read by this pass's stencil, rewritten below
@@ -743,24 +912,45 @@ static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float
       k_count_edit<false><<<148 * 8, 256, 0, C.s>>>(g, c, marks, f, C.G, xi, delta, N,
                                                     do_edit ? 1 : 0, T, C.cnt);
   });
-  C.read();
+  C.fold(buf);
   if (trk && trk->act_on) {  // act_next (| stars of `edited`) is the next pass's set
     trk->cur ^= 1;
     trk->ready = true;
     trk->edited_valid = trk->pull_stars;
   }
+  PassTicket t;
+  t.buf = buf;
+  t.listed = sparse || compact;
+  return t;
+}
+
+// The counters of an enqueued pass (waits for that pass only).
+static PassOut collect_pass(Ctx &C, const PassTicket &t) {
+  const unsigned long long *h = C.counters(t.buf);
+  if (C.prof.on) {
+    CK(cudaStreamSynchronize(C.s));
+    C.prof.drain();
+  }
   PassOut o;
-  o.vt = C.hcnt[C_VT];
-  o.applied = C.hcnt[C_APPLIED];
+  o.vt = h[C_VT];
+  o.applied = h[C_APPLIED];
   C.prof.bytes[EXACTZ_K_EDIT] += 14ull * o.applied;  // f, g, c read; g, c written
-  for (int k = 0; k < 6; ++k) o.n[k] = C.hcnt[C_N1 + k];
-  o.walk = C.hcnt[C_WALK];
+  for (int k = 0; k < 6; ++k) o.n[k] = h[C_N1 + k];
+  o.walk = h[C_WALK];
   // vertices the stencil evaluated: all of them in a dense pass, the list
   // otherwise (counted by the list / compacted stencils)
-  o.evaluated = (sparse || compact) ? C.hcnt[C_EVAL] : (unsigned long long)C.V;
-  o.links = C.hcnt[C_LINKS];
+  o.evaluated = t.listed ? h[C_EVAL] : (unsigned long long)C.V;
+  o.links = h[C_LINKS];
   C.prof.bytes[EXACTZ_K_EVENTS] += 8ull * o.links;
   return o;
+}
+
+static PassOut detect_and_edit(Ctx &C, const Reference &R, const float *f, float *g, uint8_t *c,
+                               uint32_t *marks, uint8_t *slots, uint32_t *lm, float xi,
+                               float delta, int N, uint32_t flags, bool do_edit,
+                               Tracking *trk = nullptr, int round = 0) {
+  return collect_pass(C, enqueue_pass(C, R, f, g, c, marks, slots, lm, xi, delta, N, flags,
+                                      do_edit, trk, round, 0));
 }
 
 static void validate_inputs(Ctx &C, const float *f, const float *g, float xi,
@@ -843,6 +1033,16 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   CK(cudaEventCreate(&e2));
   CK(cudaEventRecord(e0, s));
   Reference R;
+  Tracking trk;
+  trk.geometry(C);
+  // the clean-path test's f-walks (FPaths) replace the reference walks of
+  // m1 / M1 whenever list passes can run (they may use the test)
+  const bool fp_setup = !(flags & (EXACTZ_NO_TRACK | EXACTZ_REFORMULATED | EXACTZ_NO_C3 |
+                                   0x80000u | 0x100u | 0x400u));
+  auto reference = [&] {
+    build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0, fp_setup);
+    if (fp_setup) trk.start_fpaths(C, R, f);
+  };
   if (g_ready) {
     // f alone first (k_validate of (f, f) flags exactly the non-finite f),
     // its reference while g_in is still in flight, then the full check
@@ -854,14 +1054,14 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       set_err("validate", "non-finite value in f or g");
       throw Error{EXACTZ_EINVAL};
     }
-    build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
+    reference();
     CK(cudaStreamWaitEvent(s, g_ready, 0));
     validate_inputs(C, f, g_in, eps, flags);
     if (out != g_in) CK(cudaMemcpyAsync(out, g_in, V * sizeof(float), cudaMemcpyDeviceToDevice, s));
   } else {
     validate_inputs(C, f, g_in, eps, flags);
     if (out != g_in) CK(cudaMemcpyAsync(out, g_in, V * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
+    reference();
   }
   uint8_t *c = (opts && opts->edit_counts) ? opts->edit_counts : C.arena.get<uint8_t>(V);
   uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
@@ -874,8 +1074,6 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   const float delta = eps / (float)N;  // Delta = RN(xi / N)
   uint32_t it = 0, rows = 0;
   exactz_status st = EXACTZ_OK;
-  Tracking trk;
-  trk.geometry(C);
   static const unsigned long long act_div = [] {
     const char *e = std::getenv("EXACTZ_ACT_DIV");  // tuning knob (default 8)
     return e ? std::strtoull(e, nullptr, 10) : 8ull;
@@ -884,6 +1082,12 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     const char *e = std::getenv("EXACTZ_CACHE_DIV");  // tuning knob (default 4)
     return e ? std::strtoull(e, nullptr, 10) : 4ull;
   }();
+  static const double fp_gate = [] {
+    // tuning knob (default 0.05; C2 / C3 at 0, 0.15, 0.5: 37.1 / 122.8, 36.7 /
+    // 127.6, 36.9 / 134.0 ms)
+    const char *e = std::getenv("EXACTZ_FP_GATE");
+    return e ? std::atof(e) : 0.05;
+  }();
   static const unsigned long long compact_div = [] {
     const char *e = std::getenv("EXACTZ_COMPACT_DIV");  // tuning knob (default 0: off)
     return e ? std::strtoull(e, nullptr, 10) : 0ull;
@@ -891,10 +1095,30 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   unsigned long long prev_vt = (unsigned long long)V;
   const bool allow_track = !(flags & EXACTZ_NO_TRACK);
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pass_ev;
-  for (;;) {
-    bool may_edit = !(max_iters && it >= max_iters);
-    const int round = (int)rows + 1;  // stamps are 16-bit pass numbers
-    if (allow_track && rows >= 1 && round < 65000) {
+  static const bool tl = std::getenv("EXACTZ_TIMELINE") != nullptr;  // diagnostic
+  // Pipelined loop: pass r+1 is enqueued before pass r's counters are read
+  // (they arrive through mapped memory, Ctx::fold), so the host's read,
+  // decision and launches overlap the GPU's work instead of idling it
+  // between passes.  If pass r turns out to be the last (V_t = 0, or no edit
+  // applied), pass r+1 evaluated an unchanged g: it marks the same set, edits
+  // nothing, and its counters are dropped.  The tracking choices made for
+  // pass r+1 (from V_t of pass r-1) change only the speed, never the bits.
+  // Not after a pass that may not edit (max_iters: that pass is the last);
+  // off when profiling or with the per-pass timeline (debug flag 0x100000).
+  const bool pipe = !C.prof.on && !tl && !(flags & 0x100000u);
+  struct Enq {
+    PassTicket t;
+    int round = 0;
+    bool may_edit = true;
+    cudaEvent_t pa = nullptr, pb = nullptr, ta = nullptr, tb = nullptr;
+    std::chrono::steady_clock::time_point h0;
+  };
+  auto enqueue = [&](int round) {
+    Enq e;
+    e.round = round;  // stamps are 16-bit pass numbers
+    // every pass before this one edited (else the loop has ended)
+    e.may_edit = !(max_iters && (uint32_t)(round - 1) >= max_iters);
+    if (allow_track && round >= 2 && round < 65000) {
       // vertex activity once <= V/act_div vertices are marked: the pass after
       // uses the list-based sparse stencil; the C3 cache once the marks are
       // sparse at brick scale
@@ -912,6 +1136,9 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       if (!(flags & (0x200u | EXACTZ_REFORMULATED)) && !trk.cache_on &&
           prev_vt * cache_div <= (unsigned long long)trk.nb)
         trk.start_cache(C, R);
+      // the clean-path test with the list passes (debug flag 0x80000: off)
+      // (debug flag 0x200000: the test in every list pass)
+      trk.fp_gate((flags & 0x200000u) ? 0.0 : fp_gate);
     }
     // (debug 0x40000: passes after the host copy began run untracked, the
     // path a run beyond round 65000 takes)
@@ -920,21 +1147,19 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     // an untracked pass lists no edits for the host copy's patch: once the
     // copy has begun, the caller must copy the whole result instead
     if (hs && hs->started && !tracked) hs->overflow = true;
-    static const bool tl = std::getenv("EXACTZ_TIMELINE") != nullptr;  // diagnostic
-    cudaEvent_t ta = nullptr, tb = nullptr;
-    auto h0 = std::chrono::steady_clock::now();
+    e.h0 = std::chrono::steady_clock::now();
     if (tl) {
-      CK(cudaEventCreate(&ta));
-      CK(cudaEventCreate(&tb));
-      CK(cudaEventRecord(ta, s));
+      CK(cudaEventCreate(&e.ta));
+      CK(cudaEventCreate(&e.tb));
+      CK(cudaEventRecord(e.ta, s));
     }
     static const unsigned long long snap_div = [] {
-      const char *e = std::getenv("EXACTZ_SNAP_DIV");  // tuning knob (default 1024)
-      return e ? std::strtoull(e, nullptr, 10) : 1024ull;
+      const char *v = std::getenv("EXACTZ_SNAP_DIV");  // tuning knob (default 1024)
+      return v ? std::strtoull(v, nullptr, 10) : 1024ull;
     }();
     // (debug 0x10000: start as soon as vertex activity is on; 0x20000: a
     // one-entry patch list, so any later edit overflows it)
-    if (hs && !hs->started && trk.act_on && may_edit &&
+    if (hs && !hs->started && trk.act_on && e.may_edit &&
         ((flags & 0x10000u) || prev_vt * snap_div <= (unsigned long long)V)) {
       trk.patch_cap = (flags & 0x20000u) ? 1 : (int)std::min<int64_t>(V, V / 64 + 4096);
       trk.patch = C.arena.get<int32_t>(trk.patch_cap);
@@ -951,30 +1176,40 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       hs->started = true;
     }
     // per-pass GPU span for the stats rows (events read after the final sync)
-    cudaEvent_t pa = nullptr, pb = nullptr;
-    if (stats && stats->rows && rows < stats->cap) {
-      pa = pass_event();
-      pb = pass_event();
-      CK(cudaEventRecord(pa, s));
+    if (stats && stats->rows && (uint32_t)(round - 1) < stats->cap) {
+      e.pa = pass_event();
+      e.pb = pass_event();
+      CK(cudaEventRecord(e.pa, s));
     }
-    PassOut o = detect_and_edit(C, R, f, out, c, marks, slots, lm, eps, delta, N, flags, may_edit,
-                                tracked ? &trk : nullptr, round);
-    if (pa) {
-      CK(cudaEventRecord(pb, s));
-      pass_ev.push_back({pa, pb});
+    e.t = enqueue_pass(C, R, f, out, c, marks, slots, lm, eps, delta, N, flags, e.may_edit,
+                       tracked ? &trk : nullptr, round, round & 1);
+    if (e.pa) CK(cudaEventRecord(e.pb, s));
+    return e;
+  };
+  Enq cur = enqueue(1);
+  for (;;) {
+    Enq nxt;
+    bool have_next = false;
+    if (pipe && cur.may_edit) {  // speculative: cur may turn out to be the last pass
+      nxt = enqueue(cur.round + 1);
+      have_next = true;
     }
+    PassOut o = collect_pass(C, cur.t);
+    if (cur.pa) pass_ev.push_back({cur.pa, cur.pb});
     if (tl) {  // GPU span of the pass (main stream) vs host wall-clock span
-      CK(cudaEventRecord(tb, s));
-      CK(cudaEventSynchronize(tb));
+      CK(cudaEventRecord(cur.tb, s));
+      CK(cudaEventSynchronize(cur.tb));
       float gms = 0;
-      CK(cudaEventElapsedTime(&gms, ta, tb));
-      const double hms =
-          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-      std::fprintf(stderr, "pass %3d vt %12llu gpu %8.3f ms host %8.3f ms\n", round, o.vt, gms, hms);
-      cudaEventDestroy(ta);
-      cudaEventDestroy(tb);
+      CK(cudaEventElapsedTime(&gms, cur.ta, cur.tb));
+      const double hms = std::chrono::duration<double, std::milli>(
+                             std::chrono::steady_clock::now() - cur.h0).count();
+      std::fprintf(stderr, "pass %3d vt %12llu gpu %8.3f ms host %8.3f ms\n", cur.round, o.vt,
+                   gms, hms);
+      cudaEventDestroy(cur.ta);
+      cudaEventDestroy(cur.tb);
     }
     prev_vt = o.vt;
+    trk.last_n12 = o.n[0] + o.n[1];
     if (stats && stats->rows && rows < stats->cap) {
       exactz_iter_stats &r = stats->rows[rows];
       r.violations = o.vt;
@@ -986,12 +1221,22 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       r.ms = 0.0;  // set from the pass events after the final sync
     }
     ++rows;
-    if (o.vt == 0) break;
-    if (!may_edit || o.applied == 0) {
+    bool last = false;
+    if (o.vt == 0) {
+      last = true;
+    } else if (!cur.may_edit || o.applied == 0) {
       st = EXACTZ_ESTUCK;
+      last = true;
+    }
+    if (last) {
+      if (have_next && nxt.pa) {  // the dropped speculative pass
+        pass_event_put(nxt.pa);
+        pass_event_put(nxt.pb);
+      }
       break;
     }
     ++it;
+    cur = have_next ? nxt : enqueue(cur.round + 1);
   }
   CK(cudaEventRecord(e2, s));
   if (hs && hs->started) {  // patch the host copy with the vertices edited since it began

@@ -70,6 +70,7 @@ struct GridP {
   uint32_t tag[16];   // tag[k] = k
   // k_stencil_key: key of slot s = bits * 16 + kc[s], kc[s] = s - 16 bits(lo_min)
   uint32_t kc[kSlots];
+  uint32_t k16;  // 16, as a run-time value: the key products stay IMADs (stencil_key.cuh)
 };
 
 // Magic numbers of the unsigned division n / d for n < 2^31, d >= 1
@@ -81,6 +82,7 @@ inline void fastdiv_magic(uint32_t d, uint32_t &m, int &l) {
 }
 inline void grid_fastdiv(GridP &G) {
   G.keymask = ~15u;
+  G.k16 = 16u;
   for (int k = 0; k < 16; ++k) G.tag[k] = (uint32_t)k;
   fastdiv_magic((uint32_t)G.nx, G.mnx, G.lnx);
   fastdiv_magic((uint32_t)G.ny, G.mny, G.lny);
@@ -133,7 +135,18 @@ struct Track {
   int32_t *patch;
   int *npatch;
   int patch_cap;
+  // clean-path test of the C3 walks (FPaths below): tiles holding a vertex
+  // whose dn_g != dn_f (dirtD) / up_g != up_f (dirtU) in this pass, set by
+  // the list stencil (nullptr: off)
+  uint32_t *dirtD, *dirtU;  // bitmaps, bit t = tile t
+  int ntx, nty;
 };
+
+// Tiles of the clean-path test: 8 x 4 x 4 vertices.
+constexpr int FTX_SH = 3, FTY_SH = 2, FTZ_SH = 2;
+__host__ __device__ __forceinline__ int ftile(int x, int y, int z, int ntx, int nty) {
+  return (x >> FTX_SH) + ntx * ((y >> FTY_SH) + nty * (z >> FTZ_SH));
+}
 
 // Outputs of a stencil at an f-saddle i: its g-lower / g-upper link masks
 // (for the C3 walks) and its value at its position in S (for C2).
@@ -1166,6 +1179,15 @@ __device__ __forceinline__ void vertex_pass(int i, const float *__restrict__ g,
     }
   }
   for (uint32_t m = tgt; m; m &= m - 1) mark_vertex(marks, slot_target(i, __ffs(m) - 1, G), G);
+  if (T.dirtD) {  // a steepest pointer of g that is not f's: its tile is dirty (FPaths)
+    const bool dd = st.dn != ref_dn(r), du = st.up != ref_up(r);
+    if (dd || du) {
+      const int t = ftile(x, y, z, T.ntx, T.nty);
+      const uint32_t b = 1u << (t & 31);
+      if (dd && !(__ldcg(&T.dirtD[t >> 5]) & b)) atomicOr(&T.dirtD[t >> 5], b);
+      if (du && !(__ldcg(&T.dirtU[t >> 5]) & b)) atomicOr(&T.dirtU[t >> 5], b);
+    }
+  }
   const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
   if (T.bval && slots[i] != ns)  // benign race: every writer stores the same pass number
     stamp(T.bslot, T.sbslot, T, x / BX, y / BY, z / BZ, (uint16_t)T.round);
@@ -1507,14 +1529,23 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
                                                 const uint32_t *__restrict__ ref,
                                                 int32_t *ref_ext, uint32_t *marks, GridP G,
                                                 Slabs S, int32_t *remote,
-                                                unsigned long long *cnt) {
+                                                unsigned long long *cnt,
+                                                const int *__restrict__ idx = nullptr,
+                                                const int *__restrict__ nidx = nullptr) {
   __shared__ int soff[16];
   if (threadIdx.x < 16) soff[threadIdx.x] = threadIdx.x < kSlots ? slot_delta(threadIdx.x, G) : 0;
   __syncthreads();
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  // idx: the saddles to evaluate are idx[0 .. *nidx) (those the clean-path
+  // test left, k_fclean), grid-stride over a small grid; else one per thread
+  const int nact = idx ? *nidx : n;
   const int A = G.nx * G.ny, off = G.zoff * A, lo = G.zb * A, hi = G.ze * A;
   unsigned hit = 0, links = 0;
-  if (k < n) {
+#ifdef EXACTZ_WALKSTATS
+  unsigned nsteps = 0;
+#endif
+  for (int kk = blockIdx.x * blockDim.x + threadIdx.x; kk < nact;
+       kk += idx ? gridDim.x * blockDim.x : nact) {
+    const int k = idx ? __ldg(&idx[kk]) : kk;
     const int s = __ldg(&sl[k]) - off;  // local
     uint32_t todo;                       // link slots to walk from
     if (FROM_REF) {
@@ -1532,7 +1563,7 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
     } else {
       const uint32_t m = __ldg(&lm[s]);
       todo = SPLIT ? (m >> 16) : (m & 0xFFFFu);
-      links = __popc(todo);
+      links += __popc(todo);
     }
     int best = -1;
     float bv = 0.0f;
@@ -1557,6 +1588,9 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
           }
       }
       if (!runm) break;
+#ifdef EXACTZ_WALKSTATS
+      nsteps += __popc(runm);
+#endif
       int sv[KW];
 #pragma unroll
       for (int j = 0; j < KW; ++j) {
@@ -1601,13 +1635,16 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
         const int t = target - off;
         if (!SLAB || (t >= lo && t < hi)) mark_vertex(marks, t, G);
         else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = target;
-        hit = 1;
+        ++hit;  // (grid-stride over an idx list: several saddles per thread)
       }
     }
   }
   if (!FROM_REF) {
     warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
     warp_add(&cnt[C_LINKS], links);
+#ifdef EXACTZ_WALKSTATS
+    warp_add(&cnt[C_WALK], nsteps);
+#endif
   }
 }
 
@@ -1618,11 +1655,19 @@ template <bool SPLIT>
 __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict__ sl, int n,
                                                       EvCache EC, Track T, uint32_t *marks,
                                                       GridP G, int *todo, int *ntodo,
-                                                      unsigned long long *cnt) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+                                                      unsigned long long *cnt,
+                                                      const int *__restrict__ idx = nullptr,
+                                                      const int *__restrict__ nidx = nullptr) {
+  // idx: only the saddles idx[0 .. *nidx) (left by k_fclean); else all n
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  bool act = k < n;
+  if (idx) {
+    act = k < *nidx;
+    if (act) k = __ldg(&idx[k]);
+  }
   bool valid = false;
   unsigned hit = 0;
-  if (k < n) {
+  if (act) {
     const uint16_t rnd = EC.rnd[k];
     const unsigned long long mask = EC.mask[k];  // zeroed when the cache started
     valid = rnd != 0 && !(mask & kFar);
@@ -1670,7 +1715,7 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
   // (per warp, the same-address atomics queued at one L2 slice)
   __shared__ int wcnt[8], wbase[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned need = __ballot_sync(0xffffffffu, k < n && !valid);
+  const unsigned need = __ballot_sync(0xffffffffu, act && !valid);
   if (lane == 0) wcnt[wid] = __popc(need);
   __syncthreads();
   if (wid == 0) {
@@ -1720,6 +1765,9 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
   __syncthreads();
   const int n = *ntodo;
   unsigned hit = 0, links = 0;
+#ifdef EXACTZ_WALKSTATS
+  unsigned nsteps = 0;
+#endif
   if (n * 16 <= (int)(gridDim.x * blockDim.x)) {
     // few saddles (late passes: mostly long walks that never stay cached):
     // 16 lanes per saddle, one walk per lane, for the shortest critical path
@@ -1765,6 +1813,9 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
           }
       }
       if (!runm) break;
+#ifdef EXACTZ_WALKSTATS
+      nsteps += __popc(runm);
+#endif
       int sv[2];
 #pragma unroll
       for (int j = 0; j < 2; ++j)
@@ -1804,6 +1855,286 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
   }
   warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
   warp_add(&cnt[C_LINKS], links);
+#ifdef EXACTZ_WALKSTATS
+  warp_add(&cnt[C_WALK], nsteps);
+#endif
+}
+
+// ------------------------------------------- clean-path test (NEXT-2)
+// Incremental labels (P:309 and P:581 name path tracing
+// as the cost).  If no vertex on the f-walks from the f-lower link of a join
+// saddle s has dn_g != dn_f, and L_g(s) = L_f(s), then every g-walk of R5 is
+// the f-walk from the same vertex, so X = {lab_dn_g(u) : u in L_g(s)} is the
+// set X_f of the f-labels, computed once here, and m2 = max_<g X_f needs the
+// g-values of its few elements only (no walk).  Split saddles likewise with
+// up pointers and U.  "Dirty" is tested per 8x4x4 tile: the list stencil
+// flags the tiles of the vertices whose g-pointer differs from f's (a vertex
+// not evaluated in a list pass did not fire in its last evaluation, so its
+// pointers are f's).  The tiles each saddle's f-walks visit are listed once.
+constexpr int kFLab = 8;  // distinct f-labels kept per saddle (more: always walked)
+struct FPaths {
+  const int64_t *off;    // [n] first tile entry of each saddle (a warp's 32 lists are contiguous)
+  const uint16_t *len;   // [n] its number of tile entries
+  const int32_t *tiles;  // tiles visited by the f-walks (consecutive repeats dropped)
+  const int32_t *lab;    // [n * kFLab] the distinct f-termini X_f
+  const uint8_t *nlab;   // [n] |X_f|, 255 when more than kFLab
+  const unsigned long long *bmask;  // [n] bricks of the star and the f-walks (EvCache format)
+  const uint32_t *dirt;  // [ntiles bits] this pass's dirty tiles (dirtD / dirtU)
+  int nt;                // ntiles
+};
+
+// Setup: the f-walks of every saddle of the list, from its f-lower (join) /
+// f-upper (split) link along f's steepest slots (ref word), one thread per
+// saddle: m1 / M1 (ext; the reference of P:298-299, in place of k_events'
+// FROM_REF walks), the tiles visited (buffered per thread, at most kFTileCap; longer
+// lists, or a full tile array, make the saddle "always walked"), X_f, and the
+// bricks of its star and walks for the brick-stamp cache.  A warp reserves
+// one contiguous run for its 32 lists (k_fclean scans it coalesced).
+constexpr int kFTileCap = 512;
+static_assert(kFTileCap <= 65535, "FPaths::len is 16-bit");
+template <bool SPLIT>
+__global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, int n,
+                                                const uint32_t *__restrict__ ref, GridP G,
+                                                int ntx, int nty, unsigned long long *bump,
+                                                unsigned long long cap, int64_t *off,
+                                                uint16_t *len, int32_t *tiles, int32_t *lab,
+                                                uint8_t *nlab, unsigned long long *bmask,
+                                                unsigned long long *diag,
+                                                const float *__restrict__ f, int32_t *ext) {
+  __shared__ int soff[16], sdel[16];  // linear offset; packed (dx+1, dy+1, dz+1)
+  if (threadIdx.x < 16) {
+    const int q = threadIdx.x;
+    soff[q] = q < kSlots ? slot_delta(q, G) : 0;
+    int p = 1 | (1 << 2) | (1 << 4);
+    if (q < kSlots) {
+      const int b = slot_bits(q), sg1 = slot_sign(q);
+      p = (1 + sg1 * (b & 1)) | ((1 + sg1 * ((b >> 1) & 1)) << 2) | ((1 + sg1 * (b >> 2)) << 4);
+    }
+    sdel[q] = p;
+  }
+  __syncthreads();
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = k < n;
+  int32_t buf[kFTileCap];
+  int e = 0, nl = 0;
+  int best = -1;  // m1 (join) / M1 (split): the SoS-extreme terminus
+  float bv = 0.0f;
+  int lb[kFLab];
+#pragma unroll
+  for (int j = 0; j < kFLab; ++j) lb[j] = -1;
+  unsigned long long mask = 0;
+  if (act) {
+    const int s = __ldg(&sl[k]);
+    const int yz = div_nx(s, G), sz = div_ny(yz, G);
+    const int sx = s - yz * G.nx, sy = yz - sz * G.ny;
+    const uint32_t valid = valid_mask(sx, sy, sz, G), flow = ref_flow(__ldg(&ref[s]));
+    // bricks a cached result of s depends on while its walks are f's (as
+    // k_events_cached records them): the closed star and every walked vertex
+    // (tiles nest in bricks: one brick bit per new tile)
+    const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
+    brick_bit(sx, sy, sz, bsx, bsy, bsz, mask);
+    for (uint32_t v = valid; v; v &= v - 1) {
+      const int p = sdel[__ffs(v) - 1];
+      brick_bit(sx + (p & 3) - 1, sy + ((p >> 2) & 3) - 1, sz + (p >> 4) - 1, bsx, bsy, bsz, mask);
+    }
+    int last = -1, last2 = -1;  // the last two tiles listed (walks of one saddle overlap)
+    for (uint32_t todo = SPLIT ? (valid & ~flow) : flow; todo; todo &= todo - 1) {
+      const int q = __ffs(todo) - 1;
+      int p = sdel[q], w = s + soff[q];
+      int x = sx + (p & 3) - 1, y = sy + ((p >> 2) & 3) - 1, z = sz + (p >> 4) - 1;
+      for (;;) {
+        const int t = ftile(x, y, z, ntx, nty);
+        if (t != last && t != last2) {
+          if (e < kFTileCap) buf[e] = t;
+          ++e;
+          last2 = last;
+          last = t;
+          brick_bit(x, y, z, bsx, bsy, bsz, mask);
+        }
+        const int sv = (__ldg(&ref[w]) >> (SPLIT ? 18 : 14)) & 15;
+        if (sv == kSelf) break;
+        p = sdel[sv];
+        w += soff[sv];
+        x += (p & 3) - 1;
+        y += ((p >> 2) & 3) - 1;
+        z += (p >> 4) - 1;
+      }
+      {
+        const float val = f[w];
+        bool take;
+        if (best < 0) take = true;
+        else if (!SPLIT) take = (bv < val) || (bv == val && best < w);  // SoS max
+        else take = (val < bv) || (val == bv && w < best);               // SoS min
+        if (take) { best = w; bv = val; }
+      }
+      bool seen = false;
+#pragma unroll
+      for (int j = 0; j < kFLab; ++j) seen |= lb[j] == w;
+      if (!seen) {
+#pragma unroll
+        for (int j = 0; j < kFLab; ++j)
+          if (j == nl) lb[j] = w;
+        ++nl;
+      }
+    }
+  }
+  // one reservation per warp, lists in lane order
+  const int lane = threadIdx.x & 31;
+  // (a reserved run holds no holes: k_fclean scans the warp's run whole)
+  const bool want = act && e <= kFTileCap && nl <= kFLab;
+  const int c = want ? e : 0;
+  int inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  const int tot = __shfl_sync(0xffffffffu, inc, 31);
+  unsigned long long base = 0;
+  if (lane == 0 && tot) base = atomicAdd(bump, (unsigned long long)tot);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const bool fits = base + (unsigned long long)tot <= cap;
+  if (!act) return;
+  const bool ok = fits && want;
+  if (diag) {  // saddles left to the walks: list too long, too many labels, array full; entries
+    if (e > kFTileCap) atomicAdd(&diag[0], 1ull);
+    if (nl > kFLab) atomicAdd(&diag[1], 1ull);
+    if (want && !fits) atomicAdd(&diag[2], 1ull);
+    if (ok) atomicAdd(&diag[3], (unsigned long long)e);
+  }
+  const unsigned long long o0 = base + (unsigned long long)(inc - c);
+  if (ok)
+    for (int j = 0; j < e; ++j) tiles[o0 + j] = buf[j];
+  off[k] = (int64_t)o0;
+  len[k] = (uint16_t)(ok ? e : 0);
+  bmask[k] = mask;
+  nlab[k] = (uint8_t)(ok ? nl : 255);  // 255: always walked
+#pragma unroll
+  for (int j = 0; j < kFLab; ++j) lab[(size_t)k * kFLab + j] = lb[j];
+  ext[k] = best;
+}
+
+// CTA-aggregated append of k to todo for the threads with `need` (one atomic
+// per CTA; any block size <= 1024).  Every thread of the block must call it.
+__device__ __forceinline__ void cta_append(bool need, int k, int *todo, int *ntodo) {
+  __shared__ int wcnt[32], wbase[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, need);
+  if (lane == 0) wcnt[wid] = __popc(m);
+  __syncthreads();
+  if (wid == 0) {
+    const int c = lane < nw ? wcnt[lane] : 0;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, inc, 31);
+    int base = 0;
+    if (lane == 0 && tot) base = atomicAdd(ntodo, tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane < nw) wbase[lane] = base + inc - c;
+  }
+  __syncthreads();
+  if ((m >> lane) & 1u) todo[wbase[wid] + __popc(m & ((1u << lane) - 1u))] = k;
+  __syncthreads();  // wcnt / wbase are reused by the next call
+}
+
+// Per pass: a saddle whose link partition is f's and whose f-walk tiles are
+// all clean takes X = X_f (R5 / R6 without walks); the others are listed in
+// todo for the walk kernels.  idx: only the saddles idx[0 .. *nidx) (those
+// the brick-stamp cache left, k_events_check); EC.rnd: a clean saddle's
+// result is cached with the bricks of its star and f-walks (its g-walks), so
+// later passes re-emit it while those bricks are unchanged.  Grid-stride
+// (block-uniform trip count): a launch over a short idx list stays small.
+template <bool SPLIT>
+__global__ void __launch_bounds__(256) k_fclean(const float *__restrict__ g,
+                                                const int32_t *__restrict__ sl, int n,
+                                                const uint32_t *__restrict__ lm,
+                                                const uint32_t *__restrict__ ref, FPaths F,
+                                                const int32_t *__restrict__ ref_ext,
+                                                uint32_t *marks, GridP G, int *todo, int *ntodo,
+                                                unsigned long long *cnt,
+                                                const int *__restrict__ idx,
+                                                const int *__restrict__ nidx, EvCache EC,
+                                                int round) {
+  auto dirty = [&](int t) -> uint32_t { return (__ldg(&F.dirt[t >> 5]) >> (t & 31)) & 1u; };
+  const int lane = threadIdx.x & 31;
+  const int nact = idx ? *nidx : n;
+  unsigned hit = 0;
+  // block-uniform trip count (cta_append synchronises the block)
+  for (int base = blockIdx.x * blockDim.x; base < nact; base += gridDim.x * blockDim.x) {
+    const int kk = base + threadIdx.x;
+    const bool act = kk < nact;
+    const int k = act ? (idx ? __ldg(&idx[kk]) : kk) : 0;
+    bool need = false;
+    int s = 0, nl = 0;
+    if (act) {
+      s = __ldg(&sl[k]);
+      nl = F.nlab[k];
+      need = nl > kFLab || ((__ldg(&lm[s]) ^ __ldg(&ref[s])) & 0x3FFFu) != 0;
+    }
+    if (!idx) {
+      // the warp's 32 saddles own one contiguous run of tile entries: scan it
+      // 32 entries at a time (coalesced), each lane testing the dirty entries
+      // of the window against its own range
+      const int64_t o0 = act ? F.off[k] : 0, o1 = act ? o0 + F.len[k] : 0;
+      const int64_t E0 = __shfl_sync(0xffffffffu, o0, 0);
+      const int64_t E1 =
+          (int64_t)__reduce_max_sync(0xffffffffu, act ? (unsigned)(o1 - E0) : 0u) + E0;
+      for (int64_t eb = E0; eb < E1; eb += 32) {
+        if (__all_sync(0xffffffffu, need || !act)) break;
+        const int64_t e = eb + lane;
+        const bool d = e < E1 && dirty(__ldg(&F.tiles[e]));
+        const unsigned D = __ballot_sync(0xffffffffu, d);
+        if (D && act && !need) {
+          const int64_t lo = o0 > eb ? o0 : eb, hi = o1 < eb + 32 ? o1 : eb + 32;
+          if (lo < hi) {
+            const int a = (int)(lo - eb), b = (int)(hi - eb);
+            const unsigned rm = (b >= 32 ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << a) - 1u);
+            need = (D & rm) != 0;
+          }
+        }
+      }
+    } else if (act && !need) {
+      const int64_t e0 = F.off[k], e1 = e0 + F.len[k];
+      for (int64_t e = e0; e < e1 && !need; e += 4) {  // four tiles in flight
+        uint32_t d = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (e + j < e1) d |= dirty(__ldg(&F.tiles[e + j]));
+        need = d != 0;
+      }
+    }
+    if (act && !need) {
+      int best = -1;
+      float bv = 0.0f;
+      for (int j = 0; j < nl; ++j) {
+        const int lab = __ldg(&F.lab[(size_t)k * kFLab + j]);
+        const float val = g[lab];
+        bool take;
+        if (best < 0) take = true;
+        else if (!SPLIT) take = (bv < val) || (bv == val && best < lab);  // SoS max
+        else take = (val < bv) || (val == bv && lab < best);               // SoS min
+        if (take) { best = lab; bv = val; }
+      }
+      const int want = __ldg(&ref_ext[k]);
+      int target = -1;
+      if (best >= 0 && best != want) {
+        target = SPLIT ? want : best;
+        mark_vertex(marks, target, G);
+        ++hit;
+      }
+      if (EC.rnd) {
+        EC.rnd[k] = (uint16_t)round;
+        EC.mask[k] = F.bmask[k];
+        EC.tgt[k] = target;
+      }
+    }
+    cta_append(act && need, k, todo, ntodo);
+  }
+  warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
 }
 
 // ------------------------------------------------ sharded helpers (z-slabs)

@@ -347,15 +347,18 @@ struct KeyOut {
 
 // R1-R3 of one vertex from its 14 neighbour value bits (slot order) and
 // centre bits hb (see the header of this file)
+// k16: 16 as a kernel-parameter value the compiler cannot fold (callers),
+// so the 14 key products stay IMADs (FMA pipe) instead of LEAs on the ALU
+// pipe that bounds the kernel
 __device__ __forceinline__ KeyOut key_rules(const uint32_t (&bv)[kSlots], uint32_t hb,
                                             uint32_t valid, bool edge_warp, uint32_t r,
                                             const GridP &G, unsigned &n1, unsigned &n2,
-                                            unsigned &n3) {
+                                            unsigned &n3, uint32_t k16 = 16u) {
   uint32_t kmax, kmin;
   {
     uint32_t k[kSlots];
 #pragma unroll
-    for (int s = 0; s < kSlots; ++s) k[s] = bv[s] * 16u + G.kc[s];
+    for (int s = 0; s < kSlots; ++s) k[s] = bv[s] * k16 + G.kc[s];
     if (edge_warp) {
       uint32_t km[kSlots];
 #pragma unroll
@@ -510,6 +513,7 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
   // (FMA pipe) instead of becoming a shift on the busier ALU pipe
   uint32_t ptx = 1u << tx;
   asm volatile("mov.b32 %0, %0;" : "+r"(ptx));
+  const uint32_t k16 = G.k16;  // likewise for the key products (key_rules)
   unsigned n1 = 0, n2 = 0, n3 = 0;
   const int A = G.nx * G.ny;
   auto slot_of = [&](int p) { return (p - z0 + 1) & 3; };  // ring slot of plane p
@@ -635,14 +639,14 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
     KeyOut oa, ob;
     {
       const uint32_t bv[kSlots] = {mmm, m0m, mm0, m00, cmm, c0m, cm0, c10, c01, c11, p00, p10, p01, p11};
-      oa = key_rules(bv, c00, va, edge, cur.ra, G, m1, m2, m3);
+      oa = key_rules(bv, c00, va, edge, cur.ra, G, m1, m2, m3, k16);
     }
     if (!ina) { oa.tgt = 0; m1 = m2 = m3 = 0; }
     n1 += m1; n2 += m2; n3 += m3;
     m1 = m2 = m3 = 0;
     {
       const uint32_t bv[kSlots] = {mm0, m00, mm1, m01, cm0, c00, cm1, c11, c02, c12, p01, p11, p02, p12};
-      ob = key_rules(bv, c01, vb, edge, cur.rb, G, m1, m2, m3);
+      ob = key_rules(bv, c01, vb, edge, cur.rb, G, m1, m2, m3, k16);
     }
     if (!inb) { ob.tgt = 0; m1 = m2 = m3 = 0; }
     n1 += m1; n2 += m2; n3 += m3;

@@ -233,17 +233,23 @@ class _one_thread:
             torch.set_num_threads(self.n)
 
 
-def make(config: str, device="cpu", shape=None, mode: str = "uniform"):
+def make(config: str, device="cpu", shape=None, mode: str = "uniform", seed_offset: int = 0,
+         xi: float | None = None):
     """(f, ghat, xi) for a config id; `shape` overrides the 3D shape (scaled
     samples with the same recipe).  On the CPU the bytes are host- and
-    thread-count-independent (see _one_thread)."""
+    thread-count-independent (see _one_thread).  seed_offset: an independent
+    field of the same recipe (weak scaling: one per rank); xi: the bound to
+    decompress with instead of the field's own rel * range (the same xi on
+    every rank of a weak-scaling run)."""
     with _one_thread(device):
-        return _make(config, device, shape, mode)
+        return _make(config, device, shape, mode, seed_offset, xi)
 
 
-def _make(config, device, shape, mode):
+def _make(config, device, shape, mode, seed_offset=0, xi=None):
     c = CONFIGS[config]
     kw = dict(c["kw"])
+    if seed_offset:
+        kw["seed"] = kw["seed"] + 1000 * seed_offset
     if shape is not None:
         if c["gen"] == "gaussmix":
             kw["n"] = shape[0]
@@ -253,6 +259,7 @@ def _make(config, device, shape, mode):
             kw["shape"] = tuple(shape)
     kw["rel"] = c["rel"]
     f = _GENS[c["gen"]](device=device, **kw)
-    xi = xi_from_rel(f, c["rel"])
-    g = decompress(f, xi, c["seed"], mode=mode)
+    if xi is None:
+        xi = xi_from_rel(f, c["rel"])
+    g = decompress(f, xi, c["seed"] + seed_offset, mode=mode)
     return f.contiguous(), g.contiguous(), xi

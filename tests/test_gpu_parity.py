@@ -255,8 +255,10 @@ def test_repeat_bit_identical(exactz):
 
 # debug flags of exactz_correct (exactz.cu correct_impl): 0x400 compacted
 # stencil passes from the second pass on (never the sparse one), 0x200 no C3
-# cache, 0x100 no vertex activity
-TRACK_MODES = [0, 0x400, 0x400 | 0x200, 0x100]
+# cache, 0x100 no vertex activity, 0x80000 no clean-path test (FPaths)
+NO_FPATHS, FPATHS_ALWAYS = 0x80000, 0x200000  # (the gate of the test off: every list pass)
+TRACK_MODES = [0, 0x400, 0x400 | 0x200, 0x100, 0x200, NO_FPATHS, NO_FPATHS | 0x200,
+               FPATHS_ALWAYS, FPATHS_ALWAYS | 0x200]
 
 
 @pytest.mark.parametrize("mode", TRACK_MODES)
@@ -346,3 +348,18 @@ def test_host_entry_rejects_bad_outputs(exactz):
                {"label_max": torch.empty(f.numel(), dtype=torch.int32, device="cuda")}):
         with pytest.raises(ValueError):
             E.exactz_correct_host(f, g, xi, **kw)
+
+
+@pytest.mark.parametrize("cfg,shape,mode", [("C3", (33, 40, 150), None), ("C2", (40, 48, 200), None),
+                                            ("C3", (12, 16, 140), "sz"), ("C4", (1, 300, 700), None)])
+def test_clean_path_test_engages(exactz, oracle, cfg, shape, mode):
+    """NEXT-2 incremental labels: in list passes the saddles whose f-walks
+    cross no tile with a non-f pointer take X_f without walking (k_fclean).
+    Bit-exact with the oracle, and the walks it saves are visible in the
+    per-pass link counts (vertices walked from)."""
+    f, g, xi = S.make(cfg, shape=shape, mode=mode or "uniform")
+    ro, rg, c, lmin, lmax = run_both(exactz, oracle, f, g, xi, gpu_flags=FPATHS_ALWAYS)
+    assert_parity(ro, rg, c, lmin, lmax)
+    b = exactz.exactz_correct(f.cuda(), g.cuda(), xi, flags=NO_FPATHS, stats_cap=100000)
+    assert b.stats == rg.stats and b.iters == rg.iters
+    assert sum(rg.pass_links) < sum(b.pass_links), (sum(rg.pass_links), sum(b.pass_links))

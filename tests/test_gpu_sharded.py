@@ -96,3 +96,25 @@ def test_slabs_negative_values_in_one_slab(exactz, oracle):
     r = oracle.correct(f.numpy(), g.numpy(), xi, 5)
     assert b.iters == r.iters and b.status == r.status
     assert np.array_equal(b.out.cpu().numpy().reshape(-1).view(np.uint32), r.out.view(np.uint32))
+
+
+@pytest.mark.parametrize("cfg,shape", [("C1", None), ("C2", (20, 24, 70)), ("C3", (17, 21, 40))])
+def test_nccl_transport_one_rank(exactz, cfg, shape):
+    """The NCCL data plane itself (exactz_correct_sharded over a real NCCL
+    communicator: ncclSend/Recv of ghost planes and marks, all-gathers of the
+    boundary tables, all-reduces of the counters) on the one GPU of the box as
+    a 1-rank communicator: bit-equal to exactz_correct."""
+    f, g, xi = S.make(cfg, shape=shape)
+    fd, gd = f.cuda(), g.cuda()
+    c1 = torch.empty(f.numel(), dtype=torch.uint8, device="cuda")
+    c2 = torch.empty_like(c1)
+    a = exactz.exactz_correct(fd, gd, xi, edit_counts=c1, stats_cap=100000)
+    comm = exactz.Comm(exactz.exactz_nccl_unique_id(), 1, 0, torch.cuda.current_device())
+    try:
+        dims = (f.shape[2], f.shape[1], f.shape[0])
+        b = exactz.exactz_correct_sharded(comm, fd, gd, dims, xi, edit_counts=c2,
+                                          stats_cap=100000)
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    assert_same(a, b, c1, c2)

@@ -66,3 +66,21 @@ def test_szlike_roundtrip():
         e4 = Z.encode(f, xi, g2)
         assert e4["n_exc"] == 4
         assert torch.equal(Z.decode(e4).view(torch.int32), g2.view(torch.int32))
+
+
+def test_weak_scaling_fields():
+    """bench.py --scaling weak: one field per rank (seed offset), decompressed
+    with a common xi (the smallest rank's): distinct fields, every bound held,
+    min f >= xi on every rank (no lo-collapse)."""
+    xs = [S.make("C2", shape=(16, 16, 24), seed_offset=r)[2] for r in range(3)]
+    xi = min(xs)
+    fs = []
+    for r in range(3):
+        f, g, x = S.make("C2", shape=(16, 16, 24), seed_offset=r, xi=xi)
+        assert x == xi
+        assert float((f.double() - g.double()).abs().max()) <= xi
+        assert float(f.min()) >= xi
+        fs.append(f)
+    assert not torch.equal(fs[0], fs[1]) and not torch.equal(fs[1], fs[2])
+    f0, _, _ = S.make("C2", shape=(16, 16, 24))
+    assert torch.equal(f0, S.make("C2", shape=(16, 16, 24), seed_offset=0)[0])

@@ -1,18 +1,25 @@
+"""Dev bisect: tracked vs dense (NO_TRACK) runs, first differing per-pass row, per debug flag.
+
+    python tools/cmp_track.py C3 [shape ...]     (shape like 128x128x128; none: full size)"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from synth import fields as S
 import paper_2604_01397_b200 as E
-for cfg, shape in [("C1", None), ("C4", (1, 300, 700)), ("C2", (40, 48, 200))]:
+FLAGS = [(0, "default"), (0x80000, "no fpaths"), (0x200000, "fpaths always"),
+         (0x100000, "no pipelining"), (0x200, "no cache"), (0x200 | 0x200000, "fp always, no cache"),
+         (0x80000 | 0x100000, "no fp, no pipe")]
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
+shapes = [tuple(int(x) for x in a.split("x")) if a else None for a in sys.argv[2:]] or [None]
+for shape in shapes:
     f, g, xi = S.make(cfg, shape=shape, device="cuda")
     ref = E.exactz_correct(f, g, xi, flags=E.NO_TRACK, stats_cap=10000)
-    refr = E.exactz_correct(f, g, xi, flags=E.NO_TRACK | E.REFORMULATED, stats_cap=10000)
-    for fl, name in [(0x200, "act only"), (0x100, "cache only"), (0, "both"), (0x10, "reform")]:
+    for fl, name in FLAGS:
         r = E.exactz_correct(f, g, xi, flags=fl, stats_cap=10000)
-        if fl == 0x10: ref_, ref = ref, refr
         same = torch.equal(r.out.view(torch.int32), ref.out.view(torch.int32))
         first = next((k for k, (a, b) in enumerate(zip(r.stats, ref.stats)) if a != b), None)
-        print(cfg, name, "status", r.status, ref.status, "iters", r.iters, ref.iters, "same", same,
-              "first diff row", first, r.stats[first] if first is not None else "",
-              ref.stats[first] if first is not None else "")
-        if fl == 0x10: ref = ref_
+        print(cfg, shape, f"{name:22s}", "iters", r.iters, ref.iters, "same", same, "first diff row",
+              first, r.stats[first] if first is not None else "",
+              ref.stats[first] if first is not None else "", flush=True)
+    del f, g
+    torch.cuda.empty_cache()

@@ -17,6 +17,8 @@ for rep in range(int(os.environ.get("REPS", "3"))):
     r = E.exactz_correct(f, g, xi, stats_cap=10000)
     s1.record(); torch.cuda.synchronize()
     ms = s0.elapsed_time(s1)
-    print(f"rep {rep} status {r.status} iters {r.iters} ms {ms:.1f} setup {r.ms_setup:.1f} loop {r.ms_loop:.1f} GB/s {4*f.numel()/ms/1e6:.2f}", flush=True)
+    spans = sum(r.pass_ms) if getattr(r, "pass_ms", None) else float("nan")
+    print(f"rep {rep} status {r.status} iters {r.iters} ms {ms:.2f} setup {r.ms_setup:.2f} loop {r.ms_loop:.2f} "
+          f"pass spans {spans:.2f} (gaps {r.ms_loop - spans:.2f}) GB/s {4*f.numel()/ms/1e6:.2f}", flush=True)
 print("first rows", r.stats[:3])
 print("last rows", r.stats[-3:])
