@@ -413,6 +413,8 @@ struct Reference {
   int nC = 0;
   int32_t *posS = nullptr;  // [V]: position in S of each f-saddle (other entries unused)
   uint32_t *gS = nullptr;   // [nS]: g at S[k] (value bits), written by the stencils
+  uint32_t *lmS = nullptr;  // [nS]: g link masks of S[k], written by the stencils
+  int32_t *Jpos = nullptr, *Ppos = nullptr;  // [nJ] / [nP]: positions in S of J[k] / P[k]
 };
 
 // Sort 64-bit SoS keys (ordered(f) << 32 | idx) and keep the indices.
@@ -451,7 +453,9 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
                           const uint32_t *lm, const uint32_t *ref, int32_t *ext, uint32_t *marks,
                           EvCache ec = EvCache{}, Track tr = Track{}, int *todo = nullptr,
                           int *ntodo = nullptr, FPaths fp = FPaths{}, int *ftodo = nullptr,
-                          int *nftodo = nullptr) {
+                          int *nftodo = nullptr, const int32_t *lpos = nullptr) {
+  ec.lpos = lpos;
+  fp.lpos = lpos;
   if (n <= 0) return;
   const int64_t threads = n;  // one lane per saddle
   // algorithmic bytes: 8 per saddle (id, m1 / M1) here, 8 per
@@ -476,7 +480,7 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
     C.run(cls, 8ull * n, true, [&] {
       k_events<SPLIT, FROM_REF, false><<<grid, 256, 0, C.s>>>(
           h, sl, n, slots, lm, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt,
-          idx, nidx);
+          idx, nidx, lpos);
     });
     return;
   }
@@ -553,6 +557,7 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
     // C2 by saddle values in S order: posS for the stencils' writes of gS
     R.posS = C.arena.get<int32_t>((size_t)V);
     R.gS = C.arena.get<uint32_t>(R.nS);
+    R.lmS = C.arena.get<uint32_t>(R.nS);
     C.run(EXACTZ_K_REFERENCE, 8ull * R.nS, true, [&] {
       k_scatter_pos<<<blocks_for(R.nS, 256, 1 << 30), 256, 0, C.s>>>(R.S, R.nS, R.posS);
     });
@@ -562,6 +567,13 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
     if (C.prof.on) C.prof.drain();
     R.nJ = h[0];
     R.nP = h[1];
+    // the C3 kernels read the link masks in S order through these positions
+    R.Jpos = C.arena.get<int32_t>(R.nJ);
+    R.Ppos = C.arena.get<int32_t>(R.nP);
+    C.run(EXACTZ_K_REFERENCE, 8ull * (R.nJ + R.nP), true, [&] {
+      if (R.nJ) k_gather_pos<<<blocks_for(R.nJ, 256, 1 << 30), 256, 0, C.s>>>(R.J, R.nJ, R.posS, R.Jpos);
+      if (R.nP) k_gather_pos<<<blocks_for(R.nP, 256, 1 << 30), 256, 0, C.s>>>(R.P, R.nP, R.posS, R.Ppos);
+    });
   }
   R.m1 = C.arena.get<int32_t>(R.nJ);
   R.M1 = C.arena.get<int32_t>(R.nP);
@@ -617,33 +629,35 @@ struct Tracking {
   FPaths fpJ{}, fpP{};
   uint32_t *dirtD = nullptr, *dirtU = nullptr;  // bitmaps of ntiles bits
   int *ftodo = nullptr, *ftodoP = nullptr, *nftodo = nullptr;
-  template <bool SPLIT>
-  FPaths fpaths(Ctx &C, const Reference &R, const int32_t *sl, int n, unsigned long long *bump,
-               unsigned long long *diag, const float *f, int32_t *ext) {
+  // FPaths buffers of a list (allocated on the call's stream, before the fork)
+  static FPaths fpaths_alloc(Ctx &C, int n) {
     FPaths F{};
     const size_t m = n ? (size_t)n : 1;
-    int64_t *off = C.arena.get<int64_t>(m);
-    uint16_t *len = C.arena.get<uint16_t>(m);
-    int32_t *lab = C.arena.get<int32_t>(m * kFLab);
-    uint8_t *nlab = C.arena.get<uint8_t>(m);
-    unsigned long long *bmask = C.arena.get<unsigned long long>(m);
-    // tile entries: 24 per saddle on average (C2 ~9, C3 ~?; a warp that
-    // does not fit leaves its saddles to the walks)
-    const unsigned long long cap = 24ull * m + 4096;
-    int32_t *tiles = C.arena.get<int32_t>(cap);
+    F.off = C.arena.get<int64_t>(m);
+    F.len = C.arena.get<uint16_t>(m);
+    F.lab = C.arena.get<int32_t>(m * kFLab);
+    F.nlab = C.arena.get<uint8_t>(m);
+    F.bmask = C.arena.get<unsigned long long>(m);
+    F.flow = C.arena.get<uint16_t>(m);
+    // tile entries: 24 per saddle on average (C2 7.2, C3 11.8 join / 5.2
+    // split); a warp that does not fit leaves its saddles to the walks
+    F.cap = 24ull * m + 4096;
+    F.tiles = C.arena.get<int32_t>(F.cap);
+    return F;
+  }
+  template <bool SPLIT>
+  void fpaths_launch(Ctx &C, const Reference &R, const int32_t *sl, int n, const FPaths &F,
+                     unsigned long long *bump, unsigned long long *diag, const float *f,
+                     int32_t *ext) {
     if (n > 0)
       C.run(EXACTZ_K_REFERENCE, 8ull * n, true, [&] {
         k_fpaths<SPLIT><<<(unsigned)((n + 255) / 256), 256, 0, C.s>>>(
-            sl, n, R.ref, C.G, ntx, nty, bump, cap, off, len, tiles, lab, nlab, bmask, diag, f,
-            ext);
+            sl, n, R.ref, C.G, ntx, nty, bump, F.cap, const_cast<int64_t *>(F.off),
+            const_cast<uint16_t *>(F.len), const_cast<int32_t *>(F.tiles),
+            const_cast<int32_t *>(F.lab), const_cast<uint8_t *>(F.nlab),
+            const_cast<unsigned long long *>(F.bmask), diag, f, ext,
+            const_cast<uint16_t *>(F.flow));
       });
-    F.off = off;
-    F.len = len;
-    F.tiles = tiles;
-    F.lab = lab;
-    F.nlab = nlab;
-    F.bmask = bmask;
-    return F;
   }
   // at setup, in place of the reference walks of build_reference: also
   // writes R.m1 / R.M1
@@ -663,8 +677,14 @@ struct Tracking {
       diag = C.arena.get<unsigned long long>(8);
       CK(cudaMemsetAsync(diag, 0, 8 * sizeof(unsigned long long), C.s));
     }
-    fpJ = fpaths<false>(C, R, R.J, R.nJ, bump, diag, f, R.m1);
-    fpP = fpaths<true>(C, R, R.P, R.nP, bump + 1, diag ? diag + 4 : nullptr, f, R.M1);
+    fpJ = fpaths_alloc(C, R.nJ);
+    fpP = fpaths_alloc(C, R.nP);
+    C.fork();  // the two lists concurrently
+    C.on_side(0);
+    fpaths_launch<false>(C, R, R.J, R.nJ, fpJ, bump, diag, f, R.m1);
+    C.on_side(1);
+    fpaths_launch<true>(C, R, R.P, R.nP, fpP, bump + 1, diag ? diag + 4 : nullptr, f, R.M1);
+    C.join();
     if (tl) {
       unsigned long long h[8];
       CK(cudaMemcpyAsync(h, diag, sizeof(h), cudaMemcpyDeviceToHost, C.s));
@@ -789,6 +809,7 @@ static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float
   Track T = trk ? trk->track(round) : Track{};
   T.posS = R.posS;  // the stencils write g at the saddles into gS (C2 below)
   T.gS = R.gS;
+  T.lmS = R.lmS;  // and their link masks, in S order (C3 below)
   const bool sparse = trk && trk->ready && trk->sparse;
   const bool compact = trk && trk->ready && !trk->sparse;
   // the clean-path test needs every vertex with a non-f pointer flagged: list
@@ -864,8 +885,13 @@ static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float
                                             trk->list, trk->nlist);
     });
     C.run(EXACTZ_K_SPARSE, 0, true, [&] {
-      k_stencil_list<<<148 * 16, 256, 0, C.s>>>(g, R.ref, marks, slots, lm, trk->list,
-                                                trk->nlist, C.G, T, C.cnt);
+      // (debug flag 0x400000: the float-compare list stencil for keyed fields)
+      if (C.keyed && !(flags & 0x400000u))
+        k_stencil_list_key<<<148 * 16, 256, 0, C.s>>>(g, R.ref, marks, slots, lm, trk->list,
+                                                      trk->nlist, C.G, T, C.cnt);
+      else
+        k_stencil_list<<<148 * 16, 256, 0, C.s>>>(g, R.ref, marks, slots, lm, trk->list,
+                                                  trk->nlist, C.G, T, C.cnt);
     });
   }
   // R4 (C2) from the saddle values the stencil wrote in S order (gS), and
@@ -888,17 +914,19 @@ static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float
     });
   } else if (c3 && !(flags & EXACTZ_REFORMULATED)) {
     const bool cache = trk && trk->cache_on;
-    launch_events<true, false>(C, g, R.P, R.nP, slots, lm, R.ref, R.M1, marks,
+    launch_events<true, false>(C, g, R.P, R.nP, slots, R.lmS, R.ref, R.M1, marks,
                                cache ? trk->ecP : EvCache{}, T, cache ? trk->todoP : nullptr,
                                cache ? trk->ntodo + 1 : nullptr,
                                fpass && trk->fp_use[1] ? trk->fpP : FPaths{},
-                               fpass ? trk->ftodoP : nullptr, fpass ? trk->nftodo + 1 : nullptr);
+                               fpass ? trk->ftodoP : nullptr, fpass ? trk->nftodo + 1 : nullptr,
+                               R.Ppos);
     C.on_side(0);
-    launch_events<false, false>(C, g, R.J, R.nJ, slots, lm, R.ref, R.m1, marks,
+    launch_events<false, false>(C, g, R.J, R.nJ, slots, R.lmS, R.ref, R.m1, marks,
                                 cache ? trk->ecJ : EvCache{}, T, cache ? trk->todo : nullptr,
                                 cache ? trk->ntodo : nullptr,
                                 fpass && trk->fp_use[0] ? trk->fpJ : FPaths{},
-                                fpass ? trk->ftodo : nullptr, fpass ? trk->nftodo : nullptr);
+                                fpass ? trk->ftodo : nullptr, fpass ? trk->nftodo : nullptr,
+                                R.Jpos);
   }
   C.join();
   if (trk && trk->act_on && trk->pull_stars)  // read by this pass's stencil, rewritten below
@@ -1066,7 +1094,8 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   uint8_t *c = (opts && opts->edit_counts) ? opts->edit_counts : C.arena.get<uint8_t>(V);
   uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
   uint8_t *slots = C.arena.get<uint8_t>(V);
-  uint32_t *lm = C.arena.get<uint32_t>(V);
+  // (the stencils write the saddles' link masks into R.lmS, S order)
+  uint32_t *lm = C.arena.get<uint32_t>(1);
   CK(cudaMemsetAsync(c, 0, V, s));
   CK(cudaMemsetAsync(marks, 0, C.mark_words() * sizeof(uint32_t), s));
   CK(cudaEventRecord(e1, s));
@@ -1083,10 +1112,10 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
     return e ? std::strtoull(e, nullptr, 10) : 4ull;
   }();
   static const double fp_gate = [] {
-    // tuning knob (default 0.05; C2 / C3 at 0, 0.15, 0.5: 37.1 / 122.8, 36.7 /
-    // 127.6, 36.9 / 134.0 ms)
+    // tuning knob (default 0: every list pass; medians of 9 / 6 runs, C2 / C3:
+    // gate 0 36.6 / 120.4 ms, 0.05 36.3 / 126.9, 0.15 36.5 / 126.8)
     const char *e = std::getenv("EXACTZ_FP_GATE");
-    return e ? std::atof(e) : 0.05;
+    return e ? std::atof(e) : 0.0;
   }();
   static const unsigned long long compact_div = [] {
     const char *e = std::getenv("EXACTZ_COMPACT_DIV");  // tuning knob (default 0: off)
@@ -1416,7 +1445,7 @@ exactz_status exactz_check(const float *f, const float *g, const int64_t dims[3]
     build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0);
     uint32_t *marks = C.arena.get<uint32_t>(C.mark_words());
     uint8_t *slots = C.arena.get<uint8_t>(V);
-  uint32_t *lm = C.arena.get<uint32_t>(V);
+  uint32_t *lm = C.arena.get<uint32_t>(1);  // (link masks go to R.lmS)
     CK(cudaMemsetAsync(marks, 0, C.mark_words() * sizeof(uint32_t), s));
     PassOut o = detect_and_edit(C, R, f, const_cast<float *>(g), nullptr, marks, slots, lm, eps_abs,
                                 0.0f, 5, flags, false);

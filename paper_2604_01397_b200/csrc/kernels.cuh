@@ -23,8 +23,8 @@ namespace exz {
 __constant__ LinkTables c_link = kLink;
 // Slot s decodes arithmetically (no table lookups with divergent indices):
 // b = s - 6 for s >= 7, 7 - s for s < 7; offset = sign * (b&1, (b>>1)&1, b>>2).
-__host__ __device__ __forceinline__ int slot_bits(int s) { return s >= 7 ? s - 6 : 7 - s; }
-__host__ __device__ __forceinline__ int slot_sign(int s) { return s >= 7 ? 1 : -1; }
+__host__ __device__ __forceinline__ constexpr int slot_bits(int s) { return s >= 7 ? s - 6 : 7 - s; }
+__host__ __device__ __forceinline__ constexpr int slot_sign(int s) { return s >= 7 ? 1 : -1; }
 
 // Number of connected components of the link graph induced on any subset M of
 // the 14 slots (O4), built on the host from the Kuhn tables.  The induced
@@ -71,6 +71,7 @@ struct GridP {
   // k_stencil_key: key of slot s = bits * 16 + kc[s], kc[s] = s - 16 bits(lo_min)
   uint32_t kc[kSlots];
   uint32_t k16;  // 16, as a run-time value: the key products stay IMADs (stencil_key.cuh)
+  uint32_t k2up[10];  // 2^(29 - 3r): row r of a pair layout to the top 3 bits by IMAD
 };
 
 // Magic numbers of the unsigned division n / d for n < 2^31, d >= 1
@@ -83,6 +84,7 @@ inline void fastdiv_magic(uint32_t d, uint32_t &m, int &l) {
 inline void grid_fastdiv(GridP &G) {
   G.keymask = ~15u;
   G.k16 = 16u;
+  for (int r = 0; r < 10; ++r) G.k2up[r] = 1u << (29 - 3 * r);
   for (int k = 0; k < 16; ++k) G.tag[k] = (uint32_t)k;
   fastdiv_magic((uint32_t)G.nx, G.mnx, G.lnx);
   fastdiv_magic((uint32_t)G.ny, G.mny, G.lny);
@@ -128,6 +130,8 @@ struct Track {
   uint32_t *edited;             // vertices edited by this pass (written by k_count_edit)
   const int32_t *posS;          // position in S of each f-saddle (single GPU; else nullptr)
   uint32_t *gS;                 // g at S[k] (value bits), written by the stencils for C2
+  uint32_t *lmS;                // the saddles' link masks in S order (single GPU; else the
+                                // stencils write lm[i]); read through per-list positions
   int nbx, nby, nbz, round;
   int nsx, nsy;                 // superbrick grid (x, y extents)
   // exactz_correct_host: vertices edited after the result's D2H copy began
@@ -150,10 +154,24 @@ __host__ __device__ __forceinline__ int ftile(int x, int y, int z, int ntx, int 
 
 // Outputs of a stencil at an f-saddle i: its g-lower / g-upper link masks
 // (for the C3 walks) and its value at its position in S (for C2).
+// With T.lmS (single GPU) the masks go to the saddle's position in S, a
+// compact array the C3 kernels gather from L2 instead of the V-sized lm.
 __device__ __forceinline__ void saddle_out(uint32_t *__restrict__ lm, const Track &T, int i,
                                            uint32_t lower, uint32_t valid, uint32_t vbits) {
-  lm[i] = lower | ((valid & ~lower) << 16);
-  if (T.gS) T.gS[__ldg(&T.posS[i])] = vbits;
+  const uint32_t m = lower | ((valid & ~lower) << 16);
+  if (T.gS) {
+    const int k = __ldg(&T.posS[i]);
+    T.gS[k] = vbits;
+    if (T.lmS) T.lmS[k] = m;
+    else lm[i] = m;
+  } else {
+    lm[i] = m;
+  }
+}
+// link masks of saddle k of a list (lpos: positions in S, masks in S order)
+__device__ __forceinline__ uint32_t saddle_lm(const uint32_t *__restrict__ lm,
+                                              const int32_t *__restrict__ lpos, int k, int s) {
+  return lpos ? __ldg(&lm[__ldg(&lpos[k])]) : __ldg(&lm[s]);
 }
 
 __device__ __forceinline__ void stamp(uint16_t *b, uint16_t *sb, const Track &T, int bx, int by,
@@ -1146,6 +1164,14 @@ __global__ void __launch_bounds__(256) k_act_list(uint32_t *__restrict__ act,
   }
 }
 
+__device__ __forceinline__ void vertex_outputs(int i, int x, int y, int z, int row, uint32_t r,
+                                               uint32_t valid, uint32_t tgt, uint32_t lower,
+                                               int dn, int up, const float *__restrict__ g,
+                                               uint32_t *__restrict__ marks,
+                                               uint8_t *__restrict__ slots,
+                                               uint32_t *__restrict__ lm, const GridP &G,
+                                               const Track &T);
+
 // One vertex's pass with neighbours from global memory (the list-based and
 // the direct dense passes): R1-R3, marks by atomics, slots / lm, tracking.
 __device__ __forceinline__ void vertex_pass(int i, const float *__restrict__ g,
@@ -1178,6 +1204,22 @@ __device__ __forceinline__ void vertex_pass(int i, const float *__restrict__ g,
       if (flip & ~flow) tgt |= 1u << kSelf;
     }
   }
+  vertex_outputs(i, x, y, z, row, r, valid, tgt, st.lower, st.dn, st.up, g, marks, slots, lm, G, T);
+}
+
+// The outputs of one vertex's evaluation (both list stencils): marks by
+// atomics, dirty tiles, slot byte (and its brick stamp), lm / gS at f-saddles,
+// activity for the next pass.
+__device__ __forceinline__ void vertex_outputs(int i, int x, int y, int z, int row, uint32_t r,
+                                               uint32_t valid, uint32_t tgt, uint32_t lower,
+                                               int dn, int up, const float *__restrict__ g,
+                                               uint32_t *__restrict__ marks,
+                                               uint8_t *__restrict__ slots,
+                                               uint32_t *__restrict__ lm, const GridP &G,
+                                               const Track &T) {
+  struct {
+    int dn, up;
+  } st{dn, up};
   for (uint32_t m = tgt; m; m &= m - 1) mark_vertex(marks, slot_target(i, __ffs(m) - 1, G), G);
   if (T.dirtD) {  // a steepest pointer of g that is not f's: its tile is dirty (FPaths)
     const bool dd = st.dn != ref_dn(r), du = st.up != ref_up(r);
@@ -1192,11 +1234,14 @@ __device__ __forceinline__ void vertex_pass(int i, const float *__restrict__ g,
   if (T.bval && slots[i] != ns)  // benign race: every writer stores the same pass number
     stamp(T.bslot, T.sbslot, T, x / BX, y / BY, z / BZ, (uint16_t)T.round);
   slots[i] = ns;
-  if (ref_saddle(r)) saddle_out(lm, T, i, st.lower, valid, __float_as_uint(g[i]));
+  if (ref_saddle(r)) saddle_out(lm, T, i, lower, valid, __float_as_uint(g[i]));
   if (T.act_next && tgt) atomicOr(&T.act_next[(size_t)row * G.W + (x >> 5)], 1u << (x & 31));
 }
 
-__global__ void __launch_bounds__(256) k_stencil_list(const float *__restrict__ g,
+#ifndef EXACTZ_LIST_MINB
+#define EXACTZ_LIST_MINB 6  // CTAs per SM of the list stencils (latency-bound gathers; 5 / 6 / 8: round 10 of C2 0.90 / 0.83 / 0.87 ms)
+#endif
+__global__ void __launch_bounds__(256, EXACTZ_LIST_MINB) k_stencil_list(const float *__restrict__ g,
                                                       const uint32_t *__restrict__ ref,
                                                       uint32_t *__restrict__ marks,
                                                       uint8_t *__restrict__ slots,
@@ -1252,6 +1297,12 @@ __global__ void k_saddle_order_vals(const uint32_t *__restrict__ gS,
     }
   }
   warp_add(&cnt[C_N1 + 3], n4);
+}
+
+__global__ void k_gather_pos(const int32_t *__restrict__ L, int n, const int32_t *__restrict__ pos,
+                             int32_t *out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = pos[L[k]];
 }
 
 __global__ void k_scatter_pos(const int32_t *__restrict__ S, int n, int32_t *pos) {
@@ -1362,6 +1413,7 @@ struct EvCache {
   uint16_t *rnd;
   unsigned long long *mask;
   int32_t *tgt;
+  const int32_t *lpos;  // positions in S of the list's saddles (masks in S order), or nullptr
 };
 // mask bits 0..26: bricks (dz+1)*9 + (dy+1)*3 + (dx+1) around the saddle's
 // brick; bits 32..58: superbricks likewise for vertices farther away; bit 63:
@@ -1446,7 +1498,7 @@ __device__ __forceinline__ unsigned events_group(
         const float hs = h[s], hu = h[u];
         lower = (l16 < 7) ? (hu <= hs) : (hu < hs);
       } else {
-        lower = (__ldg(&lm[s]) >> l16) & 1u;  // the stencil's g-lower mask of s
+        lower = (saddle_lm(lm, EC.lpos, k, s) >> l16) & 1u;  // the stencil's g-lower mask of s
       }
       const int bb = slot_bits(l16), sg1 = slot_sign(l16);
       const int ux = sx + sg1 * (bb & 1), uy = sy + sg1 * ((bb >> 1) & 1),
@@ -1531,7 +1583,8 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
                                                 Slabs S, int32_t *remote,
                                                 unsigned long long *cnt,
                                                 const int *__restrict__ idx = nullptr,
-                                                const int *__restrict__ nidx = nullptr) {
+                                                const int *__restrict__ nidx = nullptr,
+                                                const int32_t *__restrict__ lpos = nullptr) {
   __shared__ int soff[16];
   if (threadIdx.x < 16) soff[threadIdx.x] = threadIdx.x < kSlots ? slot_delta(threadIdx.x, G) : 0;
   __syncthreads();
@@ -1561,7 +1614,7 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
         }
       todo = SPLIT ? (valid & ~lower) : lower;
     } else {
-      const uint32_t m = __ldg(&lm[s]);
+      const uint32_t m = saddle_lm(lm, lpos, k, s);
       todo = SPLIT ? (m >> 16) : (m & 0xFFFFu);
       links += __popc(todo);
     }
@@ -1785,7 +1838,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
     const int yz = div_nx(s, G), sz = div_ny(yz, G);
     const int sx = s - yz * G.nx, sy = yz - sz * G.ny;
     const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
-    const uint32_t m = __ldg(&lm[s]);
+    const uint32_t m = saddle_lm(lm, EC.lpos, k, s);
     unsigned long long mask = 0;
     brick_bit(sx, sy, sz, bsx, bsy, bsz, mask);
     for (uint32_t v = (m | (m >> 16)) & 0x3FFFu; v; v &= v - 1) {  // the star
@@ -1879,8 +1932,11 @@ struct FPaths {
   const int32_t *lab;    // [n * kFLab] the distinct f-termini X_f
   const uint8_t *nlab;   // [n] |X_f|, 255 when more than kFLab
   const unsigned long long *bmask;  // [n] bricks of the star and the f-walks (EvCache format)
+  const uint16_t *flow;  // [n] the saddle's f-lower mask (its link partition in f)
+  const int32_t *lpos;   // positions in S (link masks in S order), or nullptr
   const uint32_t *dirt;  // [ntiles bits] this pass's dirty tiles (dirtD / dirtU)
   int nt;                // ntiles
+  unsigned long long cap;  // capacity of tiles (setup)
 };
 
 // Setup: the f-walks of every saddle of the list, from its f-lower (join) /
@@ -1900,7 +1956,8 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
                                                 uint16_t *len, int32_t *tiles, int32_t *lab,
                                                 uint8_t *nlab, unsigned long long *bmask,
                                                 unsigned long long *diag,
-                                                const float *__restrict__ f, int32_t *ext) {
+                                                const float *__restrict__ f, int32_t *ext,
+                                                uint16_t *fflow) {
   __shared__ int soff[16], sdel[16];  // linear offset; packed (dx+1, dy+1, dz+1)
   if (threadIdx.x < 16) {
     const int q = threadIdx.x;
@@ -1928,6 +1985,7 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
     const int yz = div_nx(s, G), sz = div_ny(yz, G);
     const int sx = s - yz * G.nx, sy = yz - sz * G.ny;
     const uint32_t valid = valid_mask(sx, sy, sz, G), flow = ref_flow(__ldg(&ref[s]));
+    fflow[k] = (uint16_t)flow;
     // bricks a cached result of s depends on while its walks are f's (as
     // k_events_cached records them): the closed star and every walked vertex
     // (tiles nest in bricks: one brick bit per new tile)
@@ -1938,6 +1996,8 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
       brick_bit(sx + (p & 3) - 1, sy + ((p >> 2) & 3) - 1, sz + (p >> 4) - 1, bsx, bsy, bsz, mask);
     }
     int last = -1, last2 = -1;  // the last two tiles listed (walks of one saddle overlap)
+    // one walk at a time (two in flight measured slower: C2 0.38 -> 0.51 ms,
+    // C3 8.7 -> 10.4 ms for the join list)
     for (uint32_t todo = SPLIT ? (valid & ~flow) : flow; todo; todo &= todo - 1) {
       const int q = __ffs(todo) - 1;
       int p = sdel[q], w = s + soff[q];
@@ -1959,7 +2019,7 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
         y += ((p >> 2) & 3) - 1;
         z += (p >> 4) - 1;
       }
-      {
+      {  // a terminus: m1 / M1 and X_f
         const float val = f[w];
         bool take;
         if (best < 0) take = true;
@@ -2073,7 +2133,7 @@ __global__ void __launch_bounds__(256) k_fclean(const float *__restrict__ g,
     if (act) {
       s = __ldg(&sl[k]);
       nl = F.nlab[k];
-      need = nl > kFLab || ((__ldg(&lm[s]) ^ __ldg(&ref[s])) & 0x3FFFu) != 0;
+      need = nl > kFLab || ((saddle_lm(lm, F.lpos, k, s) ^ F.flow[k]) & 0x3FFFu) != 0;
     }
     if (!idx) {
       // the warp's 32 saddles own one contiguous run of tile entries: scan it

@@ -263,7 +263,9 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
       if (TRACK && T.bval) schg = (slots[i] != ns);
       slots[i] = ns;
       if (ref_saddle(r)) {
-        lm[i] = lower | ((valid & ~lower) << 16);
+        const uint32_t m = lower | ((valid & ~lower) << 16);
+        if (T.lmS) T.lmS[pc] = m;
+        else lm[i] = m;
         if (T.gS) T.gS[pc] = bv[7];
       }
     }

@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_key(const float *__restrict__
       if (TRACK && T.bval) schg = (slots[i] != ns);
       slots[i] = ns;
       if (ref_saddle(r)) {
-        lm[i] = lower | (upper << 16);
+        if (T.lmS) T.lmS[pc] = lower | (upper << 16);
+        else lm[i] = lower | (upper << 16);
         if (T.gS) T.gS[pc] = hb;
       }
     }
@@ -409,9 +410,64 @@ __device__ __forceinline__ KeyOut key_rules(const uint32_t (&bv)[kSlots], uint32
   return o;
 }
 
+// Pair layout of the targets: a 3-bit field per combined row r (bit dx + 1),
+// vertex a's (dz, dy) rows at r = 0,1 | 3,4,5 | 7,8 and vertex b's the same
+// one row (3 bits) up, so the pair's 10 rows are C = A_a | A_b << 3.
+// k2_lay(s): the bit of slot s (14: self) in A.
+__host__ __device__ constexpr int k2_lay(int s) {
+  // slot s = sign * (b & 1, (b >> 1) & 1, b >> 2) (slot_bits / slot_sign)
+  return s == kSelf ? 13
+                    : 3 * (slot_sign(s) * (slot_bits(s) >> 2) + 1 == 0
+                               ? slot_sign(s) * ((slot_bits(s) >> 1) & 1) + 1
+                               : (slot_sign(s) * (slot_bits(s) >> 2) == 0
+                                      ? slot_sign(s) * ((slot_bits(s) >> 1) & 1) + 4
+                                      : slot_sign(s) * ((slot_bits(s) >> 1) & 1) + 7)) +
+                          slot_sign(s) * (slot_bits(s) & 1) + 1;
+}
+static_assert(k2_lay(0) == 0 && k2_lay(3) == 4 && k2_lay(4) == 9 && k2_lay(6) == 12 &&
+                  k2_lay(7) == 14 && k2_lay(9) == 17 && k2_lay(10) == 22 && k2_lay(13) == 26 &&
+                  k2_lay(kSelf) == 13,
+              "pair layout of the mark rows");
+
+// List pass on exact SoS keys (C.keyed): one listed vertex per thread, its
+// 15 values from global memory (mostly L1/L2: the list is in index order),
+// the rules of key_rules, the outputs of vertex_outputs.  Same bits as
+// k_stencil_list (the keys order like SoS, see the top of this file).
+__global__ void __launch_bounds__(256, EXACTZ_LIST_MINB) k_stencil_list_key(const float *__restrict__ g,
+                                                          const uint32_t *__restrict__ ref,
+                                                          uint32_t *__restrict__ marks,
+                                                          uint8_t *__restrict__ slots,
+                                                          uint32_t *__restrict__ lm,
+                                                          const int32_t *__restrict__ list,
+                                                          const int *__restrict__ count, GridP G,
+                                                          Track T, unsigned long long *cnt) {
+  const int n = *count;
+  const uint32_t *gb = reinterpret_cast<const uint32_t *>(g);
+  unsigned n1 = 0, n2 = 0, n3 = 0, ne = 0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int i = __ldg(&list[k]);
+    const int row = div_nx(i, G), x = i - row * G.nx;
+    const int z = div_ny(row, G), y = row - z * G.ny;
+    const uint32_t valid = valid_mask(x, y, z, G);
+    uint32_t bv[kSlots];
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) bv[s] = ((valid >> s) & 1u) ? __ldg(&gb[i + G.delta[s]]) : 0u;
+    const uint32_t r = __ldg(&ref[i]);
+    const KeyOut o = key_rules(bv, __ldg(&gb[i]), valid, valid != 0x3FFFu, r, G, n1, n2, n3,
+                               G.k16);
+    vertex_outputs(i, x, y, z, row, r, valid, o.tgt, o.lower, o.ns & 15, o.ns >> 4, g, marks,
+                   slots, lm, G, T);
+    ++ne;
+  }
+  warp_add(&cnt[C_EVAL], ne);
+  warp_add(&cnt[C_N1 + 0], n1);
+  warp_add(&cnt[C_N1 + 1], n2);
+  warp_add(&cnt[C_N1 + 2], n3);
+}
+
 // Flush plane p of k_stencil_key2's ring: lane ly = target row y0 - 1 + ly.
-// Entry words 0..9: combined rows (bit j <-> x0 - 1 + j); word 10: the
-// position-ordered targets of vertex a in lanes 30 | 31 << 16, word 11 of b.
+// Entry words 0..9: combined rows (bit j <-> x0 - 1 + j); words 10 / 11: the
+// pair layouts C of lanes 30 / 31 (their bits past x0 + 30).
 constexpr int K2WR = 16;  // mark-ring entries (steps): a flush every 8 steps reads 10
 __device__ __forceinline__ void flush_plane_key2(uint32_t *__restrict__ marks,
                                                  const uint32_t (*wr)[K2W][12], int p, int z0,
@@ -427,9 +483,7 @@ __device__ __forceinline__ void flush_plane_key2(uint32_t *__restrict__ marks,
     const int w = d >> 1, st = p - k2_dz(r);
     if (d >= 0 && !(d & 1) && w < K2W && st >= z0 && st < z1) {
       const uint32_t *e = wr[st & (K2WR - 1)][w];
-      const uint32_t ta30 = e[10] & 0xFFFFu, ta31 = e[10] >> 16;
-      const uint32_t tb30 = e[11] & 0xFFFFu, tb31 = e[11] >> 16;
-      const u64 c = ((u64)k2_row(ta30, tb30, r) << 30) | ((u64)k2_row(ta31, tb31, r) << 31);
+      const u64 c = ((u64)((e[10] >> (3 * r)) & 7u) << 30) | ((u64)((e[11] >> (3 * r)) & 7u) << 31);
       val |= (u64)e[r] | (c & ~0xFFFFFFFFull);
     }
   }
@@ -501,7 +555,17 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
   __shared__ __align__(128) uint32_t sb[4][SLOT];
   __shared__ __align__(16) uint32_t wr[K2WR][K2W][12];
   __shared__ __align__(8) uint64_t bar[4];
+  // slot-order targets -> pair layout (k2_lay): bits 0..7 and 8..14 by table
+  __shared__ uint32_t lay0[256], lay1[128];
   const int tid = threadIdx.x, tx = tid & 31, w = tid >> 5;
+  for (int m = tid; m < 256 + 128; m += TX * K2W) {
+    const int base = m < 256 ? 0 : 8, bits = m < 256 ? m : m - 256;
+    uint32_t a = 0;
+    for (int j = 0; j < 8; ++j)
+      if ((bits >> j) & 1) a |= 1u << k2_lay(base + j);
+    if (m < 256) lay0[m] = a;
+    else lay1[m - 256] = a;
+  }
   const int bx = blockIdx.x;
   const int x0 = bx * TX, y0 = blockIdx.y * K2TY;
   const int z0 = G.zb + blockIdx.z * zc, z1 = min(z0 + zc, G.ze);
@@ -655,7 +719,8 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
       if (TRACK && T.bval) schg = *slp != oa.ns;
       *slp = oa.ns;
       if (ref_saddle(cur.ra)) {
-        *lmp = oa.lower | (oa.upper << 16);
+        if (T.lmS) T.lmS[cur.pa] = oa.lower | (oa.upper << 16);
+        else *lmp = oa.lower | (oa.upper << 16);
         if (T.gS) T.gS[cur.pa] = c00;
       }
     }
@@ -663,7 +728,8 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
       if (TRACK && T.bval) schg |= slp[G.nx] != ob.ns;
       slp[G.nx] = ob.ns;
       if (ref_saddle(cur.rb)) {
-        lmp[G.nx] = ob.lower | (ob.upper << 16);
+        if (T.lmS) T.lmS[cur.pb] = ob.lower | (ob.upper << 16);
+        else lmp[G.nx] = ob.lower | (ob.upper << 16);
         if (T.gS) T.gS[cur.pb] = c01;
       }
     }
@@ -680,17 +746,18 @@ __global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__res
       if (tx == 0 && fa) atomicOr(&T.act_next[(size_t)(ya + G.ny * z) * G.W + bx], fa);
       if (tx == 0 && fb) atomicOr(&T.act_next[(size_t)(yb + G.ny * z) * G.W + bx], fb);
     }
-    // combined mark rows of the pair (position order: slots 0..6, self, 7..13)
+    // combined mark rows of the pair: the layouts by table (k2_lay), row r
+    // = bits 3r .. 3r+2 of C, placed at lane + dx + 1 by the multiply
     {
-      const uint32_t ta = (oa.tgt & 0x7Fu) | ((oa.tgt & 0x3F80u) << 1) | ((oa.tgt >> kSelf) << 7);
-      const uint32_t tb = (ob.tgt & 0x7Fu) | ((ob.tgt & 0x3F80u) << 1) | ((ob.tgt >> kSelf) << 7);
+      const uint32_t Ca = lay0[oa.tgt & 0xFFu] | lay1[oa.tgt >> 8];
+      const uint32_t Cb = lay0[ob.tgt & 0xFFu] | lay1[ob.tgt >> 8];
+      const uint32_t Cc = Ca | (Cb << 3);
       uint32_t rv[12];
 #pragma unroll
-      for (int r = 0; r < K2ROWS; ++r) rv[r] = __reduce_or_sync(0xffffffffu, k2_row(ta, tb, r) * ptx);
-      const uint32_t a30 = __shfl_sync(0xffffffffu, ta, 30), a31 = __shfl_sync(0xffffffffu, ta, 31);
-      const uint32_t b30 = __shfl_sync(0xffffffffu, tb, 30), b31 = __shfl_sync(0xffffffffu, tb, 31);
-      rv[10] = a30 | (a31 << 16);
-      rv[11] = b30 | (b31 << 16);
+      for (int r = 0; r < K2ROWS; ++r)
+        rv[r] = __reduce_or_sync(0xffffffffu, ((Cc * G.k2up[r]) >> 29) * ptx);
+      rv[10] = __shfl_sync(0xffffffffu, Cc, 30);
+      rv[11] = __shfl_sync(0xffffffffu, Cc, 31);
       if (tx == 0) {
         uint4 *d = reinterpret_cast<uint4 *>(&wr[z & (K2WR - 1)][w][0]);
         d[0] = make_uint4(rv[0], rv[1], rv[2], rv[3]);

@@ -258,7 +258,7 @@ def test_repeat_bit_identical(exactz):
 # cache, 0x100 no vertex activity, 0x80000 no clean-path test (FPaths)
 NO_FPATHS, FPATHS_ALWAYS = 0x80000, 0x200000  # (the gate of the test off: every list pass)
 TRACK_MODES = [0, 0x400, 0x400 | 0x200, 0x100, 0x200, NO_FPATHS, NO_FPATHS | 0x200,
-               FPATHS_ALWAYS, FPATHS_ALWAYS | 0x200]
+               FPATHS_ALWAYS, FPATHS_ALWAYS | 0x200, 0x400000]  # 0x400000: float list stencil
 
 
 @pytest.mark.parametrize("mode", TRACK_MODES)

@@ -14,7 +14,7 @@ print(cfg, tuple(f.shape), "xi", xi, "gen s", round(time.time() - t, 2), flush=T
 for rep in range(int(os.environ.get("REPS", "3"))):
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
-    r = E.exactz_correct(f, g, xi, stats_cap=10000)
+    r = E.exactz_correct(f, g, xi, stats_cap=10000, flags=int(os.environ.get("QT_FLAGS", "0"), 0))
     s1.record(); torch.cuda.synchronize()
     ms = s0.elapsed_time(s1)
     spans = sum(r.pass_ms) if getattr(r, "pass_ms", None) else float("nan")
