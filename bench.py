@@ -592,7 +592,9 @@ def main():
                        "l2": f"inputs {4 * V / 1e6:.0f} MB per field > 126 MB L2 (no flush)",
                        "parallelism": (f"z-slabs x{ws} (NCCL send/recv + all-gather + "
                                        "all-reduce)") if sharded else "single GPU",
-                       "edit_pct": None},
+                       "edit_pct": elog["edit_pct"] if elog else None,
+                       "mix": "worst case: uniform noise at the full amplitude xi (paper NYX: "
+                              "0.73 % of the vertices edited, P:397-402)"},
             "iterations": iters,
             "hbm_frac": roofline["frac"],
             "per_pass": per_pass,

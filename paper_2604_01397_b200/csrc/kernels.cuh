@@ -132,6 +132,10 @@ struct Track {
   uint32_t *gS;                 // g at S[k] (value bits), written by the stencils for C2
   uint32_t *lmS;                // the saddles' link masks in S order (single GPU; else the
                                 // stencils write lm[i]); read through per-list positions
+  // sharded: an entry of the replicated gS whose value changed is appended
+  // here (position, value bits) for the sparse all-gather (nullptr: off)
+  int2 *gsupd;
+  unsigned long long *ngsupd;
   int nbx, nby, nbz, round;
   int nsx, nsy;                 // superbrick grid (x, y extents)
   // exactz_correct_host: vertices edited after the result's D2H copy began
@@ -154,6 +158,19 @@ __host__ __device__ __forceinline__ int ftile(int x, int y, int z, int ntx, int 
 
 // Outputs of a stencil at an f-saddle i: its g-lower / g-upper link masks
 // (for the C3 walks) and its value at its position in S (for C2).
+// g at an f-saddle into its entry k of gS; sharded (T.gsupd), a changed
+// entry is also listed for the other ranks' replicas
+__device__ __forceinline__ void gs_write(const Track &T, int k, uint32_t vbits) {
+  if (T.gsupd) {
+    if (T.gS[k] != vbits) {
+      T.gS[k] = vbits;
+      T.gsupd[atomicAdd(T.ngsupd, 1ull)] = make_int2(k, (int)vbits);
+    }
+  } else {
+    T.gS[k] = vbits;
+  }
+}
+
 // With T.lmS (single GPU) the masks go to the saddle's position in S, a
 // compact array the C3 kernels gather from L2 instead of the V-sized lm.
 __device__ __forceinline__ void saddle_out(uint32_t *__restrict__ lm, const Track &T, int i,
@@ -161,7 +178,7 @@ __device__ __forceinline__ void saddle_out(uint32_t *__restrict__ lm, const Trac
   const uint32_t m = lower | ((valid & ~lower) << 16);
   if (T.gS) {
     const int k = __ldg(&T.posS[i]);
-    T.gS[k] = vbits;
+    gs_write(T, k, vbits);
     if (T.lmS) T.lmS[k] = m;
     else lm[i] = m;
   } else {
@@ -2226,6 +2243,21 @@ __global__ void k_fill_gS(const float *__restrict__ g, const int32_t *__restrict
   if (k >= nS) return;
   const int A = G.nx * G.ny, a = S[k] - G.zoff * A;
   gS[k] = (a >= G.zb * A && a < G.ze * A) ? __float_as_uint(g[a]) : 0u;
+}
+
+// positions in S of the saddles a slab owns (local index -> k; -1 elsewhere)
+__global__ void k_local_pos(const int32_t *__restrict__ S, int nS, int32_t *pos, GridP G) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nS) return;
+  const int A = G.nx * G.ny, a = S[k] - G.zoff * A;
+  if (a >= G.zb * A && a < G.ze * A) pos[a] = k;
+}
+// gathered (position, value bits) updates into the replicated gS (pos < 0: padding)
+__global__ void k_apply_gs(const int2 *__restrict__ upd, int n, uint32_t *gS) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int2 u = upd[k];
+  if (u.x >= 0) gS[u.x] = (uint32_t)u.y;
 }
 
 // apply gathered remote marks (global ids) that this slab owns

@@ -172,6 +172,10 @@ struct Slab {
   int32_t *CP = nullptr;  // reformulation: all critical points, replicated
   uint32_t *gC = nullptr;
   int32_t *remote = nullptr, *allremote = nullptr;
+  // sparse exchange of the replicated gS: positions in S of the owned
+  // saddles (local index), this round's changed entries, all ranks' lists
+  int32_t *posS = nullptr;
+  int2 *upd = nullptr, *allupd = nullptr;
   unsigned long long *cnt = nullptr, *hcnt = nullptr;  // device counters / host mirror
   unsigned long long *nrem = nullptr;                    // per-rank remote counts (p)
   // vertex activity (list-based passes, as exactz_correct): act[cur] = this
@@ -405,6 +409,11 @@ struct ShardedRun {
       if (nS) k_keys_to_ids<<<(nS + 255) / 256, 256, 0, s>>>(x.sorted, x.S, nS);
       x.gS = A.get<uint32_t>(std::max(nS, 1));
       x.remote = A.get<int32_t>(std::max(nS, 1));
+      x.posS = A.get<int32_t>(x.G.V);
+      CK(cudaMemsetAsync(x.posS, 0xff, (size_t)x.G.V * 4, s));
+      if (nS) k_local_pos<<<(nS + 255) / 256, 256, 0, s>>>(x.S, nS, x.posS, x.G);
+      x.upd = A.get<int2>(slot);          // at most the owned saddles
+      x.allupd = A.get<int2>(slot * p);
       // J, P: owned saddles in index order (global ids)
       const int lo = x.G.zb * (int)x.plane(), n = x.nzl * (int)x.plane();
       x.J = A.get<int32_t>(std::max<int64_t>(counts[x.rank], 1));
@@ -429,6 +438,16 @@ struct ShardedRun {
       x.M1 = A.get<int32_t>(std::max(x.nP, 1));
     });
     CK(cudaGetLastError());
+    // the replicated saddle values of the input: one full exchange (owners
+    // fill, max-all-reduce); afterwards only the entries that change travel
+    if (nS > 1) {
+      std::vector<uint32_t *> b;
+      each([&](Slab &x) {
+        k_fill_gS<<<(nS + 255) / 256, 256, 0, s>>>(x.g, x.S, nS, x.gS, x.G);
+        b.push_back(x.gS);
+      });
+      T.allreduce_max_u32(b, nS);
+    }
     if (reform) {
       gather_sorted(C_NCP, [](Slab &x) { return x.cpkeys; },
                     [](Slab &x, int32_t *ids) { x.CP = ids; }, nC);
@@ -566,14 +585,22 @@ struct ShardedRun {
   void round(bool do_edit, unsigned long long out[8]) {
     const bool c3 = !(flags & EXACTZ_NO_C3);
     zero_counters();
+    const bool c2 = !(flags & EXACTZ_NO_C2) && nS > 1;
     auto track = [&](Slab &x) {
       Track t{};
       if (act_on) {
         t.act_next = x.act[cur ^ 1];
         t.edited = x.edited;
       }
+      if (c2) {  // the stencils keep the owned entries of gS and list the changes
+        t.posS = x.posS;
+        t.gS = x.gS;
+        t.gsupd = x.upd;
+        t.ngsupd = x.nrem + p + x.rank;
+      }
       return t;
     };
+    if (c2) each([&](Slab &x) { CK(cudaMemsetAsync(x.nrem + p, 0, p * 8, s)); });
     if (act_on && ready) {  // list-based pass: fired | stars of the last pass's edits
       halo_edited();
       each([&](Slab &x) {
@@ -600,18 +627,6 @@ struct ShardedRun {
       });
     }
     CK(cudaGetLastError());
-    if (!(flags & EXACTZ_NO_C2) && nS > 1) {
-      std::vector<uint32_t *> b;
-      each([&](Slab &x) {
-        k_fill_gS<<<(nS + 255) / 256, 256, 0, s>>>(x.g, x.S, nS, x.gS, x.G);
-        b.push_back(x.gS);
-      });
-      T.allreduce_max_u32(b, nS);
-      each([&](Slab &x) {
-        k_saddle_order_slab<<<(nS + 255) / 256, 256, 0, s>>>(x.gS, x.S, nS, x.marks, x.G, x.cnt);
-      });
-      CK(cudaGetLastError());
-    }
     if (c3 && reform && nC > 1) {  // R7 on replicated critical-point values
       std::vector<uint32_t *> b;
       each([&](Slab &x) {
@@ -630,40 +645,66 @@ struct ShardedRun {
         events<false, false>(x, x.g, x.J, x.nJ, x.m1);
         events<true, false>(x, x.g, x.P, x.nP, x.M1);
       });
-      // remote targets: gather every rank's list, owners apply
+    }
+    // one count exchange for the two sparse all-gathers of the round:
+    // nrem[0, p) = each rank's remote C3 targets, nrem[p, 2p) = each rank's
+    // changed gS entries (counted by the stencils); then C2 (R4) on the
+    // updated replicas and the owners' remote marks
+    const bool c3w = c3 && !reform;
+    if (c2 || c3w) {
       std::vector<unsigned long long *> nb;
       each([&](Slab &x) {
-        CK(cudaMemsetAsync(x.nrem, 0, 2 * p * 8, s));
-        CK(cudaMemcpyAsync(x.nrem + x.rank, x.cnt + C_NREMOTE, 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemsetAsync(x.nrem, 0, p * 8, s));
+        if (c3w)
+          CK(cudaMemcpyAsync(x.nrem + x.rank, x.cnt + C_NREMOTE, 8, cudaMemcpyDeviceToDevice, s));
         nb.push_back(x.nrem);
       });
-      T.allreduce_sum_u64(nb, p);
-      std::vector<unsigned long long> counts(p);
-      CK(cudaMemcpyAsync(counts.data(), sl[0].nrem, p * 8, cudaMemcpyDeviceToHost, s));
+      T.allreduce_sum_u64(nb, 2 * p);
+      std::vector<unsigned long long> counts(2 * p);
+      CK(cudaMemcpyAsync(counts.data(), sl[0].nrem, 2 * p * 8, cudaMemcpyDeviceToHost, s));
       sync();
-      unsigned long long mx = 0, tot = 0;
+      unsigned long long mr = 0, mu = 0;
       for (int r = 0; r < p; ++r) {
-        mx = std::max(mx, counts[r]);
-        tot += counts[r];
+        mr = std::max(mr, counts[r]);
+        mu = std::max(mu, counts[p + r]);
       }
-      if (tot) {
+      if (c2 && mu) {
+        std::vector<const void *> snd;
+        std::vector<void *> rcv;
+        each([&](Slab &x) {  // pad to mu with position -1
+          if (mu > counts[p + x.rank])
+            CK(cudaMemsetAsync(x.upd + counts[p + x.rank], 0xff, (mu - counts[p + x.rank]) * 8, s));
+          snd.push_back(x.upd);
+          rcv.push_back(x.allupd);
+        });
+        T.allgather(snd, rcv, mu * 8);
+        each([&](Slab &x) {
+          const int n = (int)(mu * p);
+          k_apply_gs<<<(n + 255) / 256, 256, 0, s>>>(x.allupd, n, x.gS);
+        });
+      }
+      if (c2)
+        each([&](Slab &x) {
+          k_saddle_order_slab<<<(nS + 255) / 256, 256, 0, s>>>(x.gS, x.S, nS, x.marks, x.G, x.cnt);
+        });
+      if (c3w && mr) {
         std::vector<const void *> snd;
         std::vector<void *> rcv;
         each([&](Slab &x) {
-          int32_t *pad = A.get<int32_t>(mx);
-          CK(cudaMemsetAsync(pad, 0xff, mx * 4, s));  // -1: no vertex
+          int32_t *pad = A.get<int32_t>(mr);
+          CK(cudaMemsetAsync(pad, 0xff, mr * 4, s));  // -1: no vertex
           CK(cudaMemcpyAsync(pad, x.remote, counts[x.rank] * 4, cudaMemcpyDeviceToDevice, s));
-          x.allremote = A.get<int32_t>(mx * p);
+          x.allremote = A.get<int32_t>(mr * p);
           snd.push_back(pad);
           rcv.push_back(x.allremote);
         });
-        T.allgather(snd, rcv, mx * 4);
+        T.allgather(snd, rcv, mr * 4);
         each([&](Slab &x) {
-          const int n = (int)(mx * p);
+          const int n = (int)(mr * p);
           k_apply_remote<<<(n + 255) / 256, 256, 0, s>>>(x.allremote, n, x.marks, x.G);
         });
-        CK(cudaGetLastError());
       }
+      CK(cudaGetLastError());
     }
     // marks in the ghost planes belong to the neighbours
     {

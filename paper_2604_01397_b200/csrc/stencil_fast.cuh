@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(NT, 4) k_stencil_fast(const float *__restrict_
         const uint32_t m = lower | ((valid & ~lower) << 16);
         if (T.lmS) T.lmS[pc] = m;
         else lm[i] = m;
-        if (T.gS) T.gS[pc] = bv[7];
+        if (T.gS) gs_write(T, pc, bv[7]);
       }
     }
     if (TRACK && T.bval) {

@@ -541,8 +541,11 @@ struct K2Stage {
   static constexpr int SLOT = TMA ? 736 : K2SP;  // words per ring slot (TMA: 128-B multiple)
 };
 
+#ifndef EXACTZ_K2_MINB
+#define EXACTZ_K2_MINB 3  // CTAs per SM (80 registers)
+#endif
 template <bool TRACK, bool TMA>
-__global__ void __launch_bounds__(TX * K2W, 3) k_stencil_key2(const float *__restrict__ g,
+__global__ void __launch_bounds__(TX * K2W, EXACTZ_K2_MINB) k_stencil_key2(const float *__restrict__ g,
                                                               const uint32_t *__restrict__ ref,
                                                               uint32_t *__restrict__ marks,
                                                               uint8_t *__restrict__ slots,
