@@ -414,6 +414,7 @@ struct Reference {
   int32_t *posS = nullptr;  // [V]: position in S of each f-saddle (other entries unused)
   uint32_t *gS = nullptr;   // [nS]: g at S[k] (value bits), written by the stencils
   uint32_t *lmS = nullptr;  // [nS]: g link masks of S[k], written by the stencils
+  uint8_t *fslots = nullptr;  // [V]: dn_f | up_f << 4 (k_fpaths; nullptr: not built)
   int32_t *Jpos = nullptr, *Ppos = nullptr;  // [nJ] / [nP]: positions in S of J[k] / P[k]
 };
 
@@ -441,7 +442,7 @@ static void launch_fclean(Ctx &C, const float *h, const int32_t *sl, int n, cons
                           EvCache ec, int round) {
   const unsigned grid = idx ? 148u * 4u : (unsigned)((n + 255) / 256);
   k_fclean<SPLIT><<<grid, 256, 0, C.s>>>(h, sl, n, lm, ref, fp, ext, marks, C.G, out, nout,
-                                         C.cnt, idx, nidx, ec, round);
+                                         C.cnt, idx, nidx, ec, round, fp.ndirt, fp.max_dirt);
 }
 
 // The C3 walks of one saddle list.  fp.off (tracking, list passes): the
@@ -453,7 +454,8 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
                           const uint32_t *lm, const uint32_t *ref, int32_t *ext, uint32_t *marks,
                           EvCache ec = EvCache{}, Track tr = Track{}, int *todo = nullptr,
                           int *ntodo = nullptr, FPaths fp = FPaths{}, int *ftodo = nullptr,
-                          int *nftodo = nullptr, const int32_t *lpos = nullptr) {
+                          int *nftodo = nullptr, const int32_t *lpos = nullptr,
+                          bool dense = false) {
   ec.lpos = lpos;
   fp.lpos = lpos;
   if (n <= 0) return;
@@ -476,7 +478,9 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
   }
   if (!ec.rnd) {
     // (an idx list: a small grid-stride grid)
-    const unsigned grid = idx ? 148u * 8u : (unsigned)((threads + 255) / 256);
+    // (an idx list in a list pass: a small grid-stride grid; a dense pass,
+    // where the test is usually skipped: one thread per saddle)
+    const unsigned grid = idx && !dense ? 148u * 8u : (unsigned)((threads + 255) / 256);
     C.run(cls, 8ull * n, true, [&] {
       k_events<SPLIT, FROM_REF, false><<<grid, 256, 0, C.s>>>(
           h, sl, n, slots, lm, ref, ext, marks, C.G, Slabs{nullptr, 1, nullptr}, nullptr, C.cnt,
@@ -489,19 +493,21 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
     k_events_check<SPLIT><<<(unsigned)((n + 255) / 256), 256, 0, C.s>>>(
         sl, n, ec, tr, marks, C.G, todo, ntodo, C.cnt, idx, nidx);
   });
+  int *todo2 = nullptr, *ntodo2 = nullptr;  // the stamp check's list if k_fclean skips
   if (fp.off) {  // the clean-path test on what the stamps left (caching the clean ones)
     CK(cudaMemsetAsync(nftodo, 0, sizeof(int), C.s));
     C.run(cls, 0, true, [&] {
       launch_fclean<SPLIT>(C, h, sl, n, lm, ref, fp, ext, marks, ftodo, nftodo, todo, ntodo, ec,
                            tr.round);
     });
+    todo2 = todo;
+    ntodo2 = ntodo;
     todo = ftodo;
     ntodo = nftodo;
   }
   C.run(cls, 0, true, [&] {
     k_events_cached<SPLIT><<<148 * 16, 256, 0, C.s>>>(h, sl, todo, ntodo, slots, lm, ext, marks,
-                                                      C.G,
-                                                      ec, tr, C.cnt);
+                                                      C.G, ec, tr, C.cnt, todo2, ntodo2);
   });
 }
 
@@ -513,8 +519,10 @@ static void build_reference(Ctx &C, const float *f, Reference &R, bool reform = 
   uint64_t *keys = C.arena.get<uint64_t>(V);
   uint64_t *cpkeys = reform ? C.arena.get<uint64_t>(V) : nullptr;
   C.zero();
+  if (ext_by_fpaths) R.fslots = C.arena.get<uint8_t>(V);
   C.run(EXACTZ_K_REFERENCE, 8 * (uint64_t)V, true, [&] {
-    k_reference_tile<<<C.sgrid, 256, 0, C.s>>>(f, C.G, C.zc, R.ref, keys, cpkeys, C.cnt);
+    k_reference_tile<<<C.sgrid, 256, 0, C.s>>>(f, C.G, C.zc, R.ref, keys, cpkeys, C.cnt,
+                                               R.fslots);
   });
   C.read();
   R.nS = (int)C.hcnt[C_NSADDLE];
@@ -614,20 +622,20 @@ struct Tracking {
   int *todo = nullptr, *ntodo = nullptr, *todoP = nullptr;
   // clean-path test of the C3 walks (kernels.cuh FPaths; list passes only)
   bool fp_on = false;
-  // per pass and list (join, split): run the test only where it is expected
-  // to pay: P(a saddle is clean) ~ (1 - d)^L >= fp_gate, with d the fraction
-  // of dirty tiles (bounded by the R1 + R2 firings of the last pass read, over
-  // the tile count) and L the average tile entries per saddle
-  bool fp_use[2] = {false, false};
+  // k_fclean's gate, per list (join, split), decided on the device from this
+  // pass's dirty-tile count d: the test runs when P(a saddle is clean) ~
+  // (1 - d / ntiles)^L >= gate, L the average tile entries per saddle
   double fpL[2] = {0.0, 0.0};
-  unsigned long long last_n12 = ~0ull;
+  unsigned long long *ndirt = nullptr;  // [2] dirty tiles this pass (D, U)
   void fp_gate(double gate) {
-    const double d = nt ? std::min(1.0, (double)last_n12 / (double)nt) : 1.0;
-    for (int k = 0; k < 2; ++k) fp_use[k] = fp_on && std::pow(1.0 - d, fpL[k]) >= gate;
+    for (int k = 0; k < 2; ++k) {
+      const double f = gate > 0.0 && fpL[k] > 0.0 ? 1.0 - std::pow(gate, 1.0 / fpL[k]) : 1.0;
+      (k ? fpP : fpJ).max_dirt = gate > 0.0 ? (unsigned long long)(f * nt) : ~0ull;
+    }
   }
   int ntx = 0, nty = 0, ntz = 0, nt = 0;
   FPaths fpJ{}, fpP{};
-  uint32_t *dirtD = nullptr, *dirtU = nullptr;  // bitmaps of ntiles bits
+  uint8_t *dirtD = nullptr, *dirtU = nullptr;  // one byte per tile
   int *ftodo = nullptr, *ftodoP = nullptr, *nftodo = nullptr;
   // FPaths buffers of a list (allocated on the call's stream, before the fork)
   static FPaths fpaths_alloc(Ctx &C, int n) {
@@ -656,7 +664,7 @@ struct Tracking {
             const_cast<uint16_t *>(F.len), const_cast<int32_t *>(F.tiles),
             const_cast<int32_t *>(F.lab), const_cast<uint8_t *>(F.nlab),
             const_cast<unsigned long long *>(F.bmask), diag, f, ext,
-            const_cast<uint16_t *>(F.flow));
+            const_cast<uint16_t *>(F.flow), R.fslots);
       });
   }
   // at setup, in place of the reference walks of build_reference: also
@@ -666,9 +674,11 @@ struct Tracking {
     nty = (C.G.ny + (1 << FTY_SH) - 1) >> FTY_SH;
     ntz = (C.G.nz + (1 << FTZ_SH) - 1) >> FTZ_SH;
     nt = ntx * nty * ntz;
-    const size_t nw = ((size_t)nt + 31) / 32;
-    dirtD = C.arena.get<uint32_t>(2 * nw);
-    dirtU = dirtD + nw;
+    // the two byte arrays, then the two counts (cleared by one memset per pass)
+    const size_t nb8 = (2 * (size_t)nt + 7) / 8 * 8;
+    dirtD = C.arena.get<uint8_t>(nb8 + 16);
+    dirtU = dirtD + nt;
+    ndirt = reinterpret_cast<unsigned long long *>(dirtD + nb8);
     unsigned long long *bump = C.arena.get<unsigned long long>(2);
     CK(cudaMemsetAsync(bump, 0, 2 * sizeof(unsigned long long), C.s));
     static const bool tl = std::getenv("EXACTZ_TIMELINE") != nullptr;  // diagnostic
@@ -697,6 +707,8 @@ struct Tracking {
     fpJ.dirt = dirtD;
     fpP.dirt = dirtU;
     fpJ.nt = fpP.nt = nt;
+    fpJ.ndirt = ndirt;
+    fpP.ndirt = ndirt + 1;
     {  // average tile entries per saddle (the gate below)
       unsigned long long h[2];
       CK(cudaMemcpyAsync(h, bump, sizeof(h), cudaMemcpyDeviceToHost, C.s));
@@ -803,7 +815,8 @@ struct PassTicket {
 static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float *g, uint8_t *c,
                                uint32_t *marks, uint8_t *slots, uint32_t *lm, float xi,
                                float delta, int N, uint32_t flags, bool do_edit,
-                               Tracking *trk = nullptr, int round = 0, int buf = 0) {
+                               Tracking *trk = nullptr, int round = 0, int buf = 0,
+                               Tracking *fpk = nullptr) {
   bool c3 = !(flags & EXACTZ_NO_C3);
   C.zero();
   Track T = trk ? trk->track(round) : Track{};
@@ -812,9 +825,19 @@ static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float
   T.lmS = R.lmS;  // and their link masks, in S order (C3 below)
   const bool sparse = trk && trk->ready && trk->sparse;
   const bool compact = trk && trk->ready && !trk->sparse;
-  // the clean-path test needs every vertex with a non-f pointer flagged: list
-  // passes only (the list stencil flags; an unlisted vertex has f's pointers)
-  const bool fpass = sparse && trk->fp_on && (trk->fp_use[0] || trk->fp_use[1]);
+  // the clean-path test needs every vertex with a non-f pointer flagged: the
+  // list stencil flags them in list passes (an unlisted vertex has f's
+  // pointers).  Dense passes do not run it: flagging from the key stencil
+  // cost C3 1.8 -> 2.0 ms per dense pass and in those passes nearly every
+  // tile is dirty (the gate skipped the test in all of them)
+  const bool fpass = fpk && fpk->fp_on && sparse;
+  if (fpass) {  // this pass's dirty tiles and their counts
+    CK(cudaMemsetAsync(fpk->dirtD, 0, (2 * (size_t)fpk->nt + 7) / 8 * 8 + 16, C.s));
+    T.dirtD = fpk->dirtD;
+    T.dirtU = fpk->dirtU;
+    T.ntx = fpk->ntx;
+    T.nty = fpk->nty;
+  }
   // algorithmic bytes per vertex: g 4 + ref 4 read, slots 1 + mark bits 1/8
   // written; a sparse or compacted pass: the active vertices
   // only (plus the activity bitmap)
@@ -872,13 +895,6 @@ static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float
     });
   } else {
     CK(cudaMemsetAsync(trk->nlist, 0, sizeof(int), C.s));
-    if (fpass) {  // this pass's dirty tiles (vertex_pass)
-      CK(cudaMemsetAsync(trk->dirtD, 0, 2 * (((size_t)trk->nt + 31) / 32) * 4, C.s));
-      T.dirtD = trk->dirtD;
-      T.dirtU = trk->dirtU;
-      T.ntx = trk->ntx;
-      T.nty = trk->nty;
-    }
     C.run(EXACTZ_K_SPARSE, (uint64_t)C.V / 8, true, [&] {
       k_act_list<<<148 * 16, 256, 0, C.s>>>(trk->act[trk->cur],
                                             trk->edited_valid ? trk->edited : nullptr, C.G,
@@ -894,6 +910,10 @@ static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float
                                                   trk->nlist, C.G, T, C.cnt);
     });
   }
+  if (fpass)  // the dirty-tile counts of k_fclean's gate
+    C.run(EXACTZ_K_EVENTS, 0, true, [&] {
+      k_count_dirt<<<148 * 2, 256, 0, C.s>>>(fpk->dirtD, fpk->nt, fpk->ndirt);
+    });
   // R4 (C2) from the saddle values the stencil wrote in S order (gS), and
   // the two C3 event kernels: independent (all read the snapshot and the
   // stencil's outputs, all only OR marks and add counters); the events run
@@ -917,16 +937,16 @@ static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float
     launch_events<true, false>(C, g, R.P, R.nP, slots, R.lmS, R.ref, R.M1, marks,
                                cache ? trk->ecP : EvCache{}, T, cache ? trk->todoP : nullptr,
                                cache ? trk->ntodo + 1 : nullptr,
-                               fpass && trk->fp_use[1] ? trk->fpP : FPaths{},
-                               fpass ? trk->ftodoP : nullptr, fpass ? trk->nftodo + 1 : nullptr,
-                               R.Ppos);
+                               fpass ? fpk->fpP : FPaths{},
+                               fpass ? fpk->ftodoP : nullptr, fpass ? fpk->nftodo + 1 : nullptr,
+                               R.Ppos, !sparse && !compact);
     C.on_side(0);
     launch_events<false, false>(C, g, R.J, R.nJ, slots, R.lmS, R.ref, R.m1, marks,
                                 cache ? trk->ecJ : EvCache{}, T, cache ? trk->todo : nullptr,
                                 cache ? trk->ntodo : nullptr,
-                                fpass && trk->fp_use[0] ? trk->fpJ : FPaths{},
-                                fpass ? trk->ftodo : nullptr, fpass ? trk->nftodo : nullptr,
-                                R.Jpos);
+                                fpass ? fpk->fpJ : FPaths{},
+                                fpass ? fpk->ftodo : nullptr, fpass ? fpk->nftodo : nullptr,
+                                R.Jpos, !sparse && !compact);
   }
   C.join();
   if (trk && trk->act_on && trk->pull_stars)  // read by this pass's stencil, rewritten below
@@ -1067,9 +1087,18 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   // m1 / M1 whenever list passes can run (they may use the test)
   const bool fp_setup = !(flags & (EXACTZ_NO_TRACK | EXACTZ_REFORMULATED | EXACTZ_NO_C3 |
                                    0x80000u | 0x100u | 0x400u));
+  static const double fp_gate = [] {
+    // tuning knob (default 0.1): k_fclean runs when the estimated clean
+    // fraction (1 - dirty tiles / tiles)^L reaches it (0: always)
+    const char *e = std::getenv("EXACTZ_FP_GATE");
+    return e ? std::atof(e) : 0.1;
+  }();
   auto reference = [&] {
     build_reference(C, f, R, (flags & EXACTZ_REFORMULATED) != 0, fp_setup);
-    if (fp_setup) trk.start_fpaths(C, R, f);
+    if (fp_setup) {
+      trk.start_fpaths(C, R, f);
+      trk.fp_gate((flags & 0x200000u) ? 0.0 : fp_gate);  // (debug flag 0x200000: always)
+    }
   };
   if (g_ready) {
     // f alone first (k_validate of (f, f) flags exactly the non-finite f),
@@ -1110,12 +1139,6 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
   static const unsigned long long cache_div = [] {
     const char *e = std::getenv("EXACTZ_CACHE_DIV");  // tuning knob (default 4)
     return e ? std::strtoull(e, nullptr, 10) : 4ull;
-  }();
-  static const double fp_gate = [] {
-    // tuning knob (default 0: every list pass; medians of 9 / 6 runs, C2 / C3:
-    // gate 0 36.6 / 120.4 ms, 0.05 36.3 / 126.9, 0.15 36.5 / 126.8)
-    const char *e = std::getenv("EXACTZ_FP_GATE");
-    return e ? std::atof(e) : 0.0;
   }();
   static const unsigned long long compact_div = [] {
     const char *e = std::getenv("EXACTZ_COMPACT_DIV");  // tuning knob (default 0: off)
@@ -1166,8 +1189,6 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
           prev_vt * cache_div <= (unsigned long long)trk.nb)
         trk.start_cache(C, R);
       // the clean-path test with the list passes (debug flag 0x80000: off)
-      // (debug flag 0x200000: the test in every list pass)
-      trk.fp_gate((flags & 0x200000u) ? 0.0 : fp_gate);
     }
     // (debug 0x40000: passes after the host copy began run untracked, the
     // path a run beyond round 65000 takes)
@@ -1211,7 +1232,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       CK(cudaEventRecord(e.pa, s));
     }
     e.t = enqueue_pass(C, R, f, out, c, marks, slots, lm, eps, delta, N, flags, e.may_edit,
-                       tracked ? &trk : nullptr, round, round & 1);
+                       tracked ? &trk : nullptr, round, round & 1, &trk);
     if (e.pa) CK(cudaEventRecord(e.pb, s));
     return e;
   };
@@ -1238,7 +1259,6 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
       cudaEventDestroy(cur.tb);
     }
     prev_vt = o.vt;
-    trk.last_n12 = o.n[0] + o.n[1];
     if (stats && stats->rows && rows < stats->cap) {
       exactz_iter_stats &r = stats->rows[rows];
       r.violations = o.vt;

@@ -146,7 +146,7 @@ struct Track {
   // clean-path test of the C3 walks (FPaths below): tiles holding a vertex
   // whose dn_g != dn_f (dirtD) / up_g != up_f (dirtU) in this pass, set by
   // the list stencil (nullptr: off)
-  uint32_t *dirtD, *dirtU;  // bitmaps, bit t = tile t
+  uint8_t *dirtD, *dirtU;  // one byte per tile (plain stores of 1: no read, no atomic)
   int ntx, nty;
 };
 
@@ -485,7 +485,8 @@ __global__ void __launch_bounds__(128) k_reference(const float *__restrict__ f, 
 __global__ void __launch_bounds__(256) k_reference_tile(const float *__restrict__ f, GridP G,
                                                         int zc, uint32_t *__restrict__ ref,
                                                         uint64_t *saddle_keys, uint64_t *cp_keys,
-                                                        unsigned long long *cnt) {
+                                                        unsigned long long *cnt,
+                                                        uint8_t *__restrict__ fslots = nullptr) {
   constexpr int TXr = 32, TYr = 8, SXr = TXr + 2, SPr = SXr * (TYr + 2);
   __shared__ float sg[4][SPr];
   __shared__ unsigned wcnt[2][TYr];             // per-warp key counts of the plane
@@ -552,6 +553,9 @@ __global__ void __launch_bounds__(256) k_reference_tile(const float *__restrict_
       ref[i] = st.lower | ((uint32_t)st.dn << 14) | ((uint32_t)st.up << 18) |
                ((uint32_t)nlc << 22) | ((uint32_t)nuc << 25) | ((uint32_t)sad << 28) |
                ((uint32_t)join << 29) | ((uint32_t)split << 30);
+      // f's steepest slots as one byte (the f-walks of k_fpaths read 1 B per
+      // step instead of the 4 B ref word)
+      if (fslots) fslots[i] = (uint8_t)(st.dn | (st.up << 4));
       const uint32_t ig = (uint32_t)(i + G.zoff * G.nx * G.ny);
       key = ((uint64_t)ordered_key(*p0) << 32) | ig;
     }
@@ -1242,9 +1246,8 @@ __device__ __forceinline__ void vertex_outputs(int i, int x, int y, int z, int r
     const bool dd = st.dn != ref_dn(r), du = st.up != ref_up(r);
     if (dd || du) {
       const int t = ftile(x, y, z, T.ntx, T.nty);
-      const uint32_t b = 1u << (t & 31);
-      if (dd && !(__ldcg(&T.dirtD[t >> 5]) & b)) atomicOr(&T.dirtD[t >> 5], b);
-      if (du && !(__ldcg(&T.dirtU[t >> 5]) & b)) atomicOr(&T.dirtU[t >> 5], b);
+      if (dd) T.dirtD[t] = 1;
+      if (du) T.dirtU[t] = 1;
     }
   }
   const uint8_t ns = (uint8_t)(st.dn | (st.up << 4));
@@ -1607,14 +1610,18 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
   __syncthreads();
   // idx: the saddles to evaluate are idx[0 .. *nidx) (those the clean-path
   // test left, k_fclean), grid-stride over a small grid; else one per thread
-  const int nact = idx ? *nidx : n;
+  int nact = idx ? *nidx : n;
+  if (nact < 0) {  // the clean-path test was skipped (k_fclean's gate): every saddle
+    nact = n;
+    idx = nullptr;
+  }
   const int A = G.nx * G.ny, off = G.zoff * A, lo = G.zb * A, hi = G.ze * A;
   unsigned hit = 0, links = 0;
 #ifdef EXACTZ_WALKSTATS
   unsigned nsteps = 0;
 #endif
   for (int kk = blockIdx.x * blockDim.x + threadIdx.x; kk < nact;
-       kk += idx ? gridDim.x * blockDim.x : nact) {
+       kk += gridDim.x * blockDim.x) {
     const int k = idx ? __ldg(&idx[kk]) : kk;
     const int s = __ldg(&sl[k]) - off;  // local
     uint32_t todo;                       // link slots to walk from
@@ -1820,7 +1827,9 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
                                                        const uint32_t *__restrict__ lm,
                                                        int32_t *ref_ext, uint32_t *marks,
                                                        GridP G, EvCache EC, Track T,
-                                                       unsigned long long *cnt) {
+                                                       unsigned long long *cnt,
+                                                       const int *__restrict__ todo2 = nullptr,
+                                                       const int *__restrict__ ntodo2 = nullptr) {
   __shared__ int soff[16], sdel[16];  // linear offset; packed (dx+1, dy+1, dz+1)
   if (threadIdx.x < 16) {
     const int q = threadIdx.x;
@@ -1833,7 +1842,11 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
     sdel[q] = p;
   }
   __syncthreads();
-  const int n = *ntodo;
+  int n = *ntodo;
+  if (n < 0) {  // the clean-path test was skipped: the stamp check's list
+    todo = todo2;
+    n = *ntodo2;
+  }
   unsigned hit = 0, links = 0;
 #ifdef EXACTZ_WALKSTATS
   unsigned nsteps = 0;
@@ -1951,9 +1964,11 @@ struct FPaths {
   const unsigned long long *bmask;  // [n] bricks of the star and the f-walks (EvCache format)
   const uint16_t *flow;  // [n] the saddle's f-lower mask (its link partition in f)
   const int32_t *lpos;   // positions in S (link masks in S order), or nullptr
-  const uint32_t *dirt;  // [ntiles bits] this pass's dirty tiles (dirtD / dirtU)
+  const uint8_t *dirt;   // [ntiles] this pass's dirty tiles (dirtD / dirtU)
   int nt;                // ntiles
   unsigned long long cap;  // capacity of tiles (setup)
+  const unsigned long long *ndirt;  // dirty tiles of `dirt` this pass (device)
+  unsigned long long max_dirt;      // k_fclean's gate: skip above this many
 };
 
 // Setup: the f-walks of every saddle of the list, from its f-lower (join) /
@@ -1974,7 +1989,8 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
                                                 uint8_t *nlab, unsigned long long *bmask,
                                                 unsigned long long *diag,
                                                 const float *__restrict__ f, int32_t *ext,
-                                                uint16_t *fflow) {
+                                                uint16_t *fflow,
+                                                const uint8_t *__restrict__ fslots) {
   __shared__ int soff[16], sdel[16];  // linear offset; packed (dx+1, dy+1, dz+1)
   if (threadIdx.x < 16) {
     const int q = threadIdx.x;
@@ -2028,7 +2044,8 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
           last = t;
           brick_bit(x, y, z, bsx, bsy, bsz, mask);
         }
-        const int sv = (__ldg(&ref[w]) >> (SPLIT ? 18 : 14)) & 15;
+        const int sv = fslots ? (__ldg(&fslots[w]) >> (SPLIT ? 4 : 0)) & 15
+                              : (__ldg(&ref[w]) >> (SPLIT ? 18 : 14)) & 15;
         if (sv == kSelf) break;
         p = sdel[sv];
         w += soff[sv];
@@ -2135,8 +2152,15 @@ __global__ void __launch_bounds__(256) k_fclean(const float *__restrict__ g,
                                                 unsigned long long *cnt,
                                                 const int *__restrict__ idx,
                                                 const int *__restrict__ nidx, EvCache EC,
-                                                int round) {
-  auto dirty = [&](int t) -> uint32_t { return (__ldg(&F.dirt[t >> 5]) >> (t & 31)) & 1u; };
+                                                int round, const unsigned long long *ndirt,
+                                                unsigned long long max_dirt) {
+  // gate: with more than max_dirt dirty tiles few saddles are clean; the
+  // test is skipped and the walk kernels take every saddle (*ntodo = -1)
+  if (*ndirt > max_dirt) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ntodo = -1;
+    return;
+  }
+  auto dirty = [&](int t) -> uint32_t { return __ldg(&F.dirt[t]); };
   const int lane = threadIdx.x & 31;
   const int nact = idx ? *nidx : n;
   unsigned hit = 0;
@@ -2243,6 +2267,21 @@ __global__ void k_fill_gS(const float *__restrict__ g, const int32_t *__restrict
   if (k >= nS) return;
   const int A = G.nx * G.ny, a = S[k] - G.zoff * A;
   gS[k] = (a >= G.zb * A && a < G.ze * A) ? __float_as_uint(g[a]) : 0u;
+}
+
+// dirty tiles of this pass, D and U (k_fclean's gate): one count per list
+__global__ void k_count_dirt(const uint8_t *__restrict__ d, int nt, unsigned long long *n) {
+  unsigned a = 0, b = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    a += d[t];
+    b += d[nt + t];
+  }
+  a = __reduce_add_sync(0xffffffffu, a);
+  b = __reduce_add_sync(0xffffffffu, b);
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(&n[0], (unsigned long long)a);
+    if (b) atomicAdd(&n[1], (unsigned long long)b);
+  }
 }
 
 // positions in S of the saddles a slab owns (local index -> k; -1 elsewhere)

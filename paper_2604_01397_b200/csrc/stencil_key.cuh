@@ -344,6 +344,7 @@ struct KeyOut {
   uint32_t tgt;  // targets, slot order, bit 14 = self
   uint32_t lower, upper;
   uint8_t ns;    // dn | up << 4
+  uint32_t d;    // ns ^ (dn_f | up_f << 4): non-zero nibbles = pointers that are not f's
 };
 
 // R1-R3 of one vertex from its 14 neighbour value bits (slot order) and
@@ -407,6 +408,7 @@ __device__ __forceinline__ KeyOut key_rules(const uint32_t (&bv)[kSlots], uint32
   tgt |= (fl & flow) | ((fl & ~flow) ? (1u << kSelf) : 0u);
   o.tgt = tgt;
   o.ns = (uint8_t)ns;
+  o.d = d;
   return o;
 }
 
