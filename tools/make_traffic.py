@@ -15,9 +15,10 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-         "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+         "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
 V = 512 ** 3
-KEYS = {"stencil": "k_stencil", "events": "k_events", "list": "k_stencil_sparse",
+KEYS = {"stencil": "k_stencil", "events": "k_events", "list": "k_stencil_sparse", "fclean": "k_fclean",
         "edit": "k_edit", "order": "k_saddle_order"}
 
 
