@@ -171,6 +171,7 @@ struct Ctx {
   dim3 sgrid, sblock;                 // stencil: 32x8 columns, z chunks
   dim3 rgrid, vblock;                 // persistent row-parallel grid, 128 x-threads
   int zc = 1;
+  uint32_t dbg = 0;                   // the call's flags (debug variants of kernels)
   bool fast = false;                  // every lo >= 0: k_stencil_fast (set by validation)
   bool keyed = false;                 // value range fits exact SoS keys: k_stencil_key
   // TMA descriptor of the field the dense stencil reads (k_stencil_key2):
@@ -1073,6 +1074,7 @@ static exactz_status correct_impl(const float *f, const float *g_in, const int64
 
   Ctx C(s);
   C.V = V;
+  C.dbg = flags;
   C.prof.on = (flags & EXACTZ_PROFILE) != 0;
   C.init(dims);
   cudaEvent_t e0, e1, e2;
