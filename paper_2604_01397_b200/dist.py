@@ -13,11 +13,10 @@ import torch.distributed as dist
 
 
 def slab_of(nz: int, world: int, rank: int):
-    """Planes [z0, z0 + count) of rank: the first nz % world ranks get one extra."""
-    base, extra = divmod(nz, world)
-    count = base + (1 if rank < extra else 0)
-    z0 = rank * base + min(rank, extra)
-    return z0, count
+    """Planes [z0, z0 + count) of rank: the C ABI's split (exactz_slab_range),
+    the one source of truth (the first nz % world ranks get one extra plane)."""
+    import paper_2604_01397_b200 as E
+    return E.exactz_slab_range(nz, world, rank)
 
 
 def broadcast_uid(uid: bytes | None, group=None, device="cpu") -> bytes:

@@ -26,7 +26,9 @@ def _worker(rank, world, port, q):
         out = {}
         for nz in (1 * world, 7, 512, 560, 1024):
             z0, cnt = D.slab_of(nz, world, rank)
-            assert (z0, cnt) == E.exactz_slab_range(nz, world, rank)
+            # the split itself, restated: the first nz % world ranks get one extra plane
+            base, extra = divmod(nz, world)
+            assert (z0, cnt) == (rank * base + min(rank, extra), base + (rank < extra))
             got = [None] * world
             dist.all_gather_object(got, (z0, cnt))
             out[nz] = got
