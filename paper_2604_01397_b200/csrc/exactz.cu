@@ -466,6 +466,10 @@ static void launch_events(Ctx &C, const float *h, const int32_t *sl, int n, cons
   // the pass from the C_LINKS count
   const int cls = FROM_REF ? EXACTZ_K_REFERENCE : EXACTZ_K_EVENTS;
   const int *idx = nullptr, *nidx = nullptr;
+  if (!FROM_REF && fp.off)  // this list's dirty tiles (k_fclean's gate), on its stream
+    C.run(cls, 0, true, [&] {
+      k_count_dirt<<<148, 256, 0, C.s>>>(fp.dirt, fp.nt, const_cast<unsigned long long *>(fp.ndirt));
+    });
   if (!FROM_REF && fp.off && !ec.rnd) {
     CK(cudaMemsetAsync(nftodo, 0, sizeof(int), C.s));
     // bytes: id, lm, ref word, offsets (16 B per saddle); the tile entries
@@ -675,11 +679,12 @@ struct Tracking {
     nty = (C.G.ny + (1 << FTY_SH) - 1) >> FTY_SH;
     ntz = (C.G.nz + (1 << FTZ_SH) - 1) >> FTZ_SH;
     nt = ntx * nty * ntz;
-    // the two byte arrays, then the two counts (cleared by one memset per pass)
-    const size_t nb8 = (2 * (size_t)nt + 7) / 8 * 8;
-    dirtD = C.arena.get<uint8_t>(nb8 + 16);
-    dirtU = dirtD + nt;
-    ndirt = reinterpret_cast<unsigned long long *>(dirtD + nb8);
+    // the two byte arrays (each padded to 16 bytes), then the two counts
+    // (cleared by one memset per pass)
+    const size_t nt16 = ((size_t)nt + 15) / 16 * 16;
+    dirtD = C.arena.get<uint8_t>(2 * nt16 + 16);
+    dirtU = dirtD + nt16;
+    ndirt = reinterpret_cast<unsigned long long *>(dirtD + 2 * nt16);
     unsigned long long *bump = C.arena.get<unsigned long long>(2);
     CK(cudaMemsetAsync(bump, 0, 2 * sizeof(unsigned long long), C.s));
     static const bool tl = std::getenv("EXACTZ_TIMELINE") != nullptr;  // diagnostic
@@ -833,7 +838,7 @@ static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float
   // tile is dirty (the gate skipped the test in all of them)
   const bool fpass = fpk && fpk->fp_on && sparse;
   if (fpass) {  // this pass's dirty tiles and their counts
-    CK(cudaMemsetAsync(fpk->dirtD, 0, (2 * (size_t)fpk->nt + 7) / 8 * 8 + 16, C.s));
+    CK(cudaMemsetAsync(fpk->dirtD, 0, 2 * (((size_t)fpk->nt + 15) / 16 * 16) + 16, C.s));
     T.dirtD = fpk->dirtD;
     T.dirtU = fpk->dirtU;
     T.ntx = fpk->ntx;
@@ -911,10 +916,6 @@ static PassTicket enqueue_pass(Ctx &C, const Reference &R, const float *f, float
                                                   trk->nlist, C.G, T, C.cnt);
     });
   }
-  if (fpass)  // the dirty-tile counts of k_fclean's gate
-    C.run(EXACTZ_K_EVENTS, 0, true, [&] {
-      k_count_dirt<<<148 * 2, 256, 0, C.s>>>(fpk->dirtD, fpk->nt, fpk->ndirt);
-    });
   // R4 (C2) from the saddle values the stencil wrote in S order (gS), and
   // the two C3 event kernels: independent (all read the snapshot and the
   // stencil's outputs, all only OR marks and add counters); the events run

@@ -1131,17 +1131,22 @@ __global__ void __launch_bounds__(256) k_act_list(uint32_t *__restrict__ act,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t w0 = (int64_t)G.ny * G.zb * G.W, nwords = (int64_t)G.ny * G.ze * G.W;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // the next step's word is loaded one step ahead (the late passes are a
+  // latency-bound scan of mostly zero words)
+  uint32_t a_next = (w0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x < nwords)
+                        ? act[w0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x]
+                        : 0u;
   for (int64_t base = w0 + (int64_t)blockIdx.x * blockDim.x; base < nwords;
        base += stride) {  // block-uniform trip count
     const int64_t w = base + threadIdx.x;
-    uint32_t a = 0;
+    uint32_t a = a_next;
+    a_next = (w + stride < nwords) ? act[w + stride] : 0u;
     int row = 0, x0 = 0;
     if (w < nwords) {
       // this pass's set: fired last pass (act, consumed) | stars of its edits
       row = div_W((int)w, G);
       const int wx = (int)w - row * G.W;
       x0 = wx * 32;
-      a = act[w];
       if (a) act[w] = 0u;
       if (edited) a |= dilated_word(edited, row, wx, G);
       if (G.nx - x0 < 32) a &= (1u << (G.nx - x0)) - 1u;
@@ -2269,19 +2274,19 @@ __global__ void k_fill_gS(const float *__restrict__ g, const int32_t *__restrict
   gS[k] = (a >= G.zb * A && a < G.ze * A) ? __float_as_uint(g[a]) : 0u;
 }
 
-// dirty tiles of this pass, D and U (k_fclean's gate): one count per list
+// dirty tiles of this pass in one list's byte array (k_fclean's gate): 16
+// bytes per load (the array is padded to a multiple of 16 and zeroed)
 __global__ void k_count_dirt(const uint8_t *__restrict__ d, int nt, unsigned long long *n) {
-  unsigned a = 0, b = 0;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
-    a += d[t];
-    b += d[nt + t];
+  const uint4 *d4 = reinterpret_cast<const uint4 *>(d);
+  const int n4 = (nt + 15) / 16;
+  unsigned a = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += gridDim.x * blockDim.x) {
+    const uint4 v = __ldg(&d4[t]);  // bytes are 0 / 1: the sum of the 16 bytes
+    a += __dp4a(v.x, 0x01010101u, 0u) + __dp4a(v.y, 0x01010101u, 0u) +
+         __dp4a(v.z, 0x01010101u, 0u) + __dp4a(v.w, 0x01010101u, 0u);
   }
   a = __reduce_add_sync(0xffffffffu, a);
-  b = __reduce_add_sync(0xffffffffu, b);
-  if ((threadIdx.x & 31) == 0) {
-    if (a) atomicAdd(&n[0], (unsigned long long)a);
-    if (b) atomicAdd(&n[1], (unsigned long long)b);
-  }
+  if ((threadIdx.x & 31) == 0 && a) atomicAdd(n, (unsigned long long)a);
 }
 
 // positions in S of the saddles a slab owns (local index -> k; -1 elsewhere)
@@ -2359,12 +2364,21 @@ __global__ void __launch_bounds__(256, 8) k_count_edit(float *__restrict__ g,
                                           reinterpret_cast<uintptr_t>(g)) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(c) & 3) == 0;
   unsigned vt = 0, ap = 0;
-  for (int64_t w0 = (int64_t)G.ny * G.zb * G.W +
-                    (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
-       w0 < nwords; w0 += nwarps * 32) {
+  for (int64_t wb = (int64_t)G.ny * G.zb * G.W +
+                    (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 128;
+       wb < nwords; wb += nwarps * 128) {
+   // 4 x 32 words per warp step, loaded together (independent loads: the
+   // sparse late passes are a scan of mostly zero words, latency-bound)
+   uint32_t mine4[4];
+#pragma unroll
+   for (int q = 0; q < 4; ++q) mine4[q] = (wb + 32 * q + lane < nwords) ? marks[wb + 32 * q + lane] : 0u;
+#pragma unroll 1
+   for (int q = 0; q < 4; ++q) {
+    const int64_t w0 = wb + 32 * q;
+    if (w0 >= nwords) break;  // warp-uniform
     // 32 words per warp step (one per lane, coalesced, cleared); the non-zero
     // ones are edited four at a time, 8 lanes x 4 vertices per word
-    const uint32_t mine = (w0 + lane < nwords) ? marks[w0 + lane] : 0u;
+    const uint32_t mine = mine4[q];
     if (mine) {
       vt += __popc(mine);
       marks[w0 + lane] = 0u;
@@ -2460,6 +2474,7 @@ __global__ void __launch_bounds__(256, 8) k_count_edit(float *__restrict__ g,
         }
       }
     }
+   }
   }
   warp_add(&cnt[C_VT], vt);
   warp_add(&cnt[C_APPLIED], ap);
