@@ -1361,13 +1361,18 @@ __device__ __forceinline__ int walk(int u, const uint8_t *__restrict__ slots,
 // and last owned plane of every rank, the terminus of its steepest path in
 // the rank's slab: {label, value bits} (a root) or {-(x+1), 0} (the path
 // leaves the slab at global vertex x, which lies in a neighbour's boundary
-// plane).  Gathered on every rank and resolved by pointer jumping: paths
-// strictly descend (ascend) in SoS order, so the chains are acyclic and the
-// resolved table is unique.
+// plane).  Gathered on every rank; a lookup follows exit -> entry links to
+// the root (table_lookup): paths strictly descend (ascend) in SoS order, so
+// the chains are acyclic (they visit distinct entries; a path may cross a
+// slab border several times, in both z directions).  (r02: resolving the
+// whole gathered table on every rank each pass,
+// by a cooperative pointer-jumping kernel, was 27 % of the per-rank time of
+// an 8-slab C2 run; only the few walks that leave a slab need a chain.)
 struct Slabs {
   const int *start;  // start[r] = global first plane of rank r, start[p] = gnz
   int p;
-  const int2 *table;  // 2 * p * A resolved entries, or nullptr (single GPU)
+  const int2 *table;  // 2 * p * A entries, or nullptr (single GPU)
+  unsigned long long *err;  // set when a chain is longer than the table (never: acyclic)
 };
 
 __device__ __forceinline__ int2 table_entry(const Slabs &S, int xg, int A) {
@@ -1376,6 +1381,13 @@ __device__ __forceinline__ int2 table_entry(const Slabs &S, int xg, int A) {
   while (r + 1 < S.p && S.start[r + 1] <= z) ++r;
   const int side = (z == S.start[r]) ? 0 : 1;
   return S.table[(size_t)(2 * r + side) * A + (xg - z * A)];
+}
+__device__ __forceinline__ int2 table_lookup(const Slabs &S, int xg, int A) {
+  int2 t = table_entry(S, xg, A);
+  const int hmax = 2 * S.p * A;  // the table's entries: an acyclic chain visits each once
+  for (int h = 0; t.x < 0 && h < hmax; ++h) t = table_entry(S, -t.x - 1, A);
+  if (t.x < 0 && S.err) atomicOr(S.err, 1ull);
+  return t;
 }
 
 template <bool UP, bool FROM_REF>
@@ -1389,44 +1401,6 @@ __global__ void k_boundary_walks(const float *__restrict__ h, const uint8_t *__r
   const int e = walk<UP, FROM_REF, true>(v, slots, ref, G);
   const int off = G.zoff * A;
   out[i] = e >= 0 ? make_int2(e + off, __float_as_int(h[e])) : make_int2(-(-e - 1 + off) - 1, 0);
-}
-
-__global__ void k_resolve(int2 *table, int n, Slabs S, int A, unsigned long long *changed) {
-  unsigned ch = 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    int2 e = table[i];
-    if (e.x >= 0) continue;
-    int2 e2 = table_entry(S, -e.x - 1, A);
-    table[i] = e2;
-    ch |= (e2.x < 0);
-  }
-  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(changed, 1ull);
-}
-
-// All resolve rounds in one cooperative launch (grid-wide barriers between
-// rounds, the loop ends when no entry is still an exit): no host round trip
-// per round.  err is set when maxr rounds did not resolve every chain.
-__global__ void k_resolve_all(int2 *table, int n, Slabs S, int A, int maxr, unsigned *flag,
-                              unsigned long long *err) {
-  cg::grid_group grid = cg::this_grid();
-  for (int r = 0; r < maxr; ++r) {
-    // three flags: flag r % 3 is read after this round's barrier and reset
-    // two rounds later, after a barrier every reader has passed
-    unsigned *fl = flag + (r % 3);
-    if (grid.thread_rank() == 0) flag[(r + 1) % 3] = 0u;  // the next round's flag
-    unsigned ch = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-      int2 e = table[i];
-      if (e.x >= 0) continue;
-      int2 e2 = table_entry(S, -e.x - 1, A);
-      table[i] = e2;
-      ch |= (e2.x < 0);
-    }
-    if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(fl, 1u);
-    grid.sync();
-    if (*(volatile unsigned *)fl == 0u) return;
-  }
-  if (grid.thread_rank() == 0) *err = 1ull;
 }
 
 // Per-saddle cache of the C3 result (tracking mode).  rnd = round it was
@@ -1538,7 +1512,7 @@ __device__ __forceinline__ unsigned events_group(
           best = e + off;
           bv = h[e];
         } else {
-          const int2 t = table_entry(S, -e - 1 + off, A);
+          const int2 t = table_lookup(S, -e - 1 + off, A);
           best = t.x;
           bv = __int_as_float(t.y);
         }
@@ -1697,7 +1671,7 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
           lab = w[j] + off;
           val = h[w[j]];
         } else {
-          const int2 t = table_entry(S, w[j] + off, A);
+          const int2 t = table_lookup(S, w[j] + off, A);
           lab = t.x;
           val = __int_as_float(t.y);
         }

@@ -184,7 +184,6 @@ struct Slab {
   uint32_t *act[2] = {nullptr, nullptr}, *edited = nullptr;
   int32_t *list = nullptr;
   int *nlist = nullptr;
-  unsigned *rflag = nullptr;  // k_resolve_all round flags (3)
   size_t plane() const { return (size_t)G.nx * G.ny; }
   size_t words_per_plane() const { return (size_t)G.ny * G.W; }
 };
@@ -202,7 +201,6 @@ struct ShardedRun {
   uint32_t flags;
   bool act_on = false, ready = false;  // vertex activity started / act[cur] valid
   int cur = 0;
-  int resolve_blocks = 0;  // co-resident grid of the cooperative resolve
 
   ShardedRun(Transport &t, cudaStream_t st, Arena &a, std::vector<Slab> &slabs, int nx_, int ny_,
              int nz_, float xi_, int N_, uint32_t flags_)
@@ -273,13 +271,6 @@ struct ShardedRun {
   }
 
   void setup(const std::vector<const float *> &f_in, const std::vector<const float *> &g_in) {
-    {
-      int dev = 0, nsm = 0, per = 0;
-      CK(cudaGetDevice(&dev));
-      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_resolve_all, 256, 0));
-      resolve_blocks = nsm * (per > 4 ? 4 : (per < 1 ? 1 : per));
-    }
     int64_t gz0 = 0, gc = 0;
     std::vector<int> starts(p + 1);
     for (int r = 0; r < p; ++r) {
@@ -324,7 +315,6 @@ struct ShardedRun {
       x.cnt = A.get<unsigned long long>(C_NALLOC);
       CK(cudaMallocHost(&x.hcnt, C_NCOUNTERS * 8));
       x.nrem = A.get<unsigned long long>(2 * p);
-      x.rflag = A.get<unsigned>(3);
       x.keys = A.get<uint64_t>(x.nzl * P);
       if (reform) x.cpkeys = A.get<uint64_t>(x.nzl * P);
       x.tdn = A.get<int2>(2 * p * P);
@@ -455,17 +445,18 @@ struct ShardedRun {
       return;
     }
     // m1 / M1 from f's paths, completed across slabs
+    zero_counters();
     boundary_tables(true);
-    read_counters();
-    each([&](Slab &x) {
-      if (x.hcnt[C_CHANGED]) {
-        set_err("boundary_tables", "exit chains did not resolve");
-        throw Error{EXACTZ_ECUDA};
-      }
-    });
     each([&](Slab &x) {
       events<false, true>(x, x.f, x.J, x.nJ, x.m1);
       events<true, true>(x, x.f, x.P, x.nP, x.M1);
+    });
+    read_counters();
+    each([&](Slab &x) {
+      if (x.hcnt[C_CHANGED]) {
+        set_err("boundary_tables", "an exit chain is longer than the table (a cycle)");
+        throw Error{EXACTZ_ECUDA};
+      }
     });
   }
 
@@ -517,7 +508,9 @@ struct ShardedRun {
     CK(cudaGetLastError());
   }
 
-  Slabs slabs_of(const int2 *table) const { return Slabs{d_start, p, table}; }
+  Slabs slabs_of(const int2 *table, unsigned long long *err = nullptr) const {
+    return Slabs{d_start, p, table, err};
+  }
 
   // gather the boundary walk termini of every rank and resolve them
   void boundary_tables(bool from_ref) {
@@ -538,23 +531,7 @@ struct ShardedRun {
       });
       CK(cudaGetLastError());
       T.allgather(snd, rcv, 2 * P * sizeof(int2));
-      // every rank resolves its copy (identical inputs -> identical tables).
-      // A path crosses each slab border at most once per direction of travel
-      // (it descends strictly), so p rounds of exit -> entry replacement reach
-      // the fixpoint; one more round verifies it without a host round trip
-      // per round (the flag is read with the pass's counters).
-      each([&](Slab &x) {
-        int2 *t = up ? x.tup : x.tdn;
-        int n = (int)(2 * p * P);
-        Slabs sb = slabs_of(t);
-        int A2 = (int)P, maxr = 4 * p + 8;
-        unsigned long long *err = x.cnt + C_CHANGED;
-        CK(cudaMemsetAsync(x.rflag, 0, 3 * sizeof(unsigned), s));
-        CK(cudaMemsetAsync(err, 0, 8, s));
-        void *args[] = {&t, &n, &sb, &A2, &maxr, &x.rflag, &err};
-        CK(cudaLaunchCooperativeKernel((const void *)k_resolve_all, dim3(resolve_blocks), dim3(256),
-                                       args, 0, s));
-      });
+      // no resolve pass: lookups follow the exit chains (table_lookup)
     }
   }
 
@@ -564,7 +541,7 @@ struct ShardedRun {
     const int64_t threads = n;  // one lane per saddle
     k_events<SPLIT, FROM_REF, true><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
         h, list, n, x.slots, FROM_REF ? nullptr : x.lm, x.ref, ext, x.marks, x.G,
-        slabs_of(SPLIT ? x.tup : x.tdn), x.remote,
+        slabs_of(SPLIT ? x.tup : x.tdn, x.cnt + C_CHANGED), x.remote,
         x.cnt);
     CK(cudaGetLastError());
   }
@@ -747,7 +724,7 @@ struct ShardedRun {
     allreduce_counters();
     read_counters();
     if (c3 && !reform && sl[0].hcnt[C_CHANGED]) {  // the boundary tables' verification round
-      set_err("boundary_tables", "exit chains did not resolve");
+      set_err("boundary_tables", "an exit chain is longer than the table (a cycle)");
       throw Error{EXACTZ_ECUDA};
     }
     for (int k = 0; k < 8; ++k) out[k] = sl[0].hcnt[k];

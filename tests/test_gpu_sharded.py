@@ -118,3 +118,11 @@ def test_nccl_transport_one_rank(exactz, cfg, shape):
     finally:
         comm.close()
     assert_same(a, b, c1, c2)
+
+
+def test_slabs_long_exit_chains(exactz):
+    """A steepest path may cross a slab border several times (the value
+    descends, z need not): with 1-plane slabs the chains of boundary-table
+    exits are long; the lookups still end at the root (bit-equal)."""
+    f, g, xi = S.make("C2", shape=(12, 20, 24))
+    assert_same(*both(exactz, f, g, xi, 12))
