@@ -11,12 +11,17 @@ for cfg in sys.argv[1:]:
     f, g, xi = S.make(cfg, device="cuda")
     torch.cuda.synchronize()
     gen = time.time() - t
-    r = E.exactz_correct(f, g, xi, stats_cap=100000)  # warm
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record()
-    r = E.exactz_correct(f, g, xi, flags=E.PROFILE | int(os.environ.get("FLAGS", "0"), 0), stats_cap=100000)
-    s1.record(); torch.cuda.synchronize()
-    ms = s0.elapsed_time(s1)
+    fl = int(os.environ.get("FLAGS", "0"), 0)
+    r = E.exactz_correct(f, g, xi, stats_cap=100000, flags=fl)  # warm
+    times = []
+    for _ in range(3):  # unprofiled (the bench's path): min of 3
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        r = E.exactz_correct(f, g, xi, flags=fl, stats_cap=100000)
+        s1.record(); torch.cuda.synchronize()
+        times.append(s0.elapsed_time(s1))
+    ms = min(times)
+    r = E.exactz_correct(f, g, xi, flags=E.PROFILE | fl, stats_cap=100000)  # kernel classes
     V = f.numel()
     vt = [row[0] for row in r.stats]
     out[cfg] = dict(shape=list(f.shape), xi=xi, iters=r.iters, status=r.status, ms=ms,
