@@ -140,6 +140,48 @@ struct Kit {
 };
 static thread_local Kit g_kit;
 
+// The component LUTs of the stencils (d_comp: components of a link mask;
+// d_comp2: nlc | nuc << 3 of an interior vertex), built once per thread.
+static void upload_luts(cudaStream_t s) {
+  static thread_local uint8_t lut[1 << kSlots];
+  static thread_local uint8_t lut2[1 << kSlots];
+  static thread_local bool ready = false;
+  if (!ready) {
+    for (uint32_t m = 0; m < (1u << kSlots); ++m) lut[m] = (uint8_t)link_components_t(m, kLink.adj);
+    for (uint32_t m = 0; m < (1u << kSlots); ++m)
+      lut2[m] = (uint8_t)(lut[m] | (lut[~m & ((1u << kSlots) - 1)] << 3));
+    ready = true;
+  }
+  CK(cudaMemcpyToSymbolAsync(d_comp, lut, sizeof(lut), 0, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyToSymbolAsync(d_comp2, lut2, sizeof(lut2), 0, cudaMemcpyHostToDevice, s));
+}
+
+// TMA descriptor of a float32 field the dense key stencil reads
+// (k_stencil_key2): 3D {nx, ny, nz}, box {40, 18, 1} from x0 - 4 (the 34 x 18
+// halo tile, 16-byte aligned in x), zero fill outside the domain.  False when
+// the field does not qualify (nx % 4, alignment) or the driver call fails.
+static bool encode_plane_map(CUtensorMap *m, const void *g, int nx, int ny, int nz) {
+  if (nx % 4 != 0 || ((uintptr_t)g & 15)) return false;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!encode) return false;
+  const cuuint64_t dim[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+  const cuuint64_t stride[2] = {(cuuint64_t)nx * 4, (cuuint64_t)nx * ny * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)K2Stage<true>::SXS, (cuuint32_t)K2SY, 1},
+                   estr[3] = {1, 1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(g), dim, stride, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct Ctx {
   cudaStream_t s;
   bool kit = false;  // borrowing g_kit
@@ -181,25 +223,7 @@ struct Ctx {
   const void *tmap_ptr = nullptr;
   bool plane_map(const void *g) {
     if (g == tmap_ptr) return true;
-    if (G.nx % 4 != 0 || ((uintptr_t)g & 15) || G.zoff != 0) return false;
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-      void *fn = nullptr;
-      cudaDriverEntryPointQueryResult q;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
-              cudaSuccess ||
-          q != cudaDriverEntryPointSuccess)
-        fn = nullptr;
-      return (PFN_cuTensorMapEncodeTiled_v12000)fn;
-    }();
-    if (!encode) return false;
-    const cuuint64_t dim[3] = {(cuuint64_t)G.nx, (cuuint64_t)G.ny, (cuuint64_t)G.nz};
-    const cuuint64_t stride[2] = {(cuuint64_t)G.nx * 4, (cuuint64_t)G.nx * G.ny * 4};
-    const cuuint32_t box[3] = {(cuuint32_t)K2Stage<true>::SXS, (cuuint32_t)K2SY, 1},
-                     estr[3] = {1, 1, 1};
-    if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(g), dim, stride, box,
-               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return false;
+    if (G.zoff != 0 || !encode_plane_map(&tmap, g, G.nx, G.ny, G.nz)) return false;
     tmap_ptr = g;
     return true;
   }
@@ -327,23 +351,7 @@ struct Ctx {
     uint64_t thr = UINT64_MAX;
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   }
-  void upload_lut() {
-    static thread_local uint8_t lut[1 << kSlots];
-    static thread_local bool ready = false;
-    if (!ready) {
-      for (uint32_t m = 0; m < (1u << kSlots); ++m) lut[m] = (uint8_t)link_components_t(m, kLink.adj);
-      ready = true;
-    }
-    CK(cudaMemcpyToSymbolAsync(d_comp, lut, sizeof(lut), 0, cudaMemcpyHostToDevice, s));
-    static thread_local uint8_t lut2[1 << kSlots];
-    static thread_local bool ready2 = false;
-    if (!ready2) {
-      for (uint32_t m = 0; m < (1u << kSlots); ++m)
-        lut2[m] = (uint8_t)(lut[m] | (lut[~m & ((1u << kSlots) - 1)] << 3));
-      ready2 = true;
-    }
-    CK(cudaMemcpyToSymbolAsync(d_comp2, lut2, sizeof(lut2), 0, cudaMemcpyHostToDevice, s));
-  }
+  void upload_lut() { upload_luts(s); }
   size_t mark_words() const { return (size_t)G.ny * G.nz * G.W; }
   void zero() { CK(cudaMemsetAsync(cnt, 0, C_NALLOC * sizeof(unsigned long long), s)); }
   void read() {

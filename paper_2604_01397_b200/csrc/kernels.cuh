@@ -132,12 +132,9 @@ struct Track {
   uint32_t *gS;                 // g at S[k] (value bits), written by the stencils for C2
   uint32_t *lmS;                // the saddles' link masks in S order (single GPU; else the
                                 // stencils write lm[i]); read through per-list positions
-  // sharded: an entry of the replicated gS whose value changed is appended
-  // here (position, value bits) for the sparse all-gather (nullptr: off)
-  int2 *gsupd;
-  unsigned long long *ngsupd;
   int nbx, nby, nbz, round;
   int nsx, nsy;                 // superbrick grid (x, y extents)
+  int tab_round;                // sharded: last pass in which a boundary-table entry changed
   // exactz_correct_host: vertices edited after the result's D2H copy began
   // (patched on the host afterwards); nullptr: off
   int32_t *patch;
@@ -158,18 +155,9 @@ __host__ __device__ __forceinline__ int ftile(int x, int y, int z, int ntx, int 
 
 // Outputs of a stencil at an f-saddle i: its g-lower / g-upper link masks
 // (for the C3 walks) and its value at its position in S (for C2).
-// g at an f-saddle into its entry k of gS; sharded (T.gsupd), a changed
-// entry is also listed for the other ranks' replicas
-__device__ __forceinline__ void gs_write(const Track &T, int k, uint32_t vbits) {
-  if (T.gsupd) {
-    if (T.gS[k] != vbits) {
-      T.gS[k] = vbits;
-      T.gsupd[atomicAdd(T.ngsupd, 1ull)] = make_int2(k, (int)vbits);
-    }
-  } else {
-    T.gS[k] = vbits;
-  }
-}
+// g at an f-saddle into its entry k of gS (sharded: the changed owned
+// entries are listed afterwards by k_gs_diff)
+__device__ __forceinline__ void gs_write(const Track &T, int k, uint32_t vbits) { T.gS[k] = vbits; }
 
 // With T.lmS (single GPU) the masks go to the saddle's position in S, a
 // compact array the C3 kernels gather from L2 instead of the V-sized lm.
@@ -1418,6 +1406,10 @@ struct EvCache {
 // brick; bits 32..58: superbricks likewise for vertices farther away; bit 63:
 // a vertex outside both neighbourhoods (never reused).
 constexpr unsigned long long kFar = 1ull << 63;
+// sharded: some walk left the slab and was completed from the boundary
+// tables; the result stays valid while no table entry changed (Track.tab_round)
+constexpr unsigned long long kExit = 1ull << 62;
+constexpr uint32_t kSuperBits = 0x07FFFFFFu;  // mask bits 32..58
 
 __device__ __forceinline__ void brick_bit(int x, int y, int z, int bsx, int bsy, int bsz,
                                           unsigned long long &mask) {
@@ -1436,14 +1428,20 @@ __device__ __forceinline__ void brick_bit(int x, int y, int z, int bsx, int bsy,
     mask |= kFar;
 }
 
-// walk() that also records the bricks it visits (single GPU, g slots)
-template <bool UP>
+// walk() that also records the bricks it visits (g slots).  SLAB: a path
+// that leaves the owned planes returns -(w + 1) as walk(); the result then
+// depends on the boundary tables (kExit)
+template <bool UP, bool SLAB = false>
 __device__ __forceinline__ int walk_track(int u, int x, int y, int z,
                                           const uint8_t *__restrict__ slots, const GridP &G,
                                           int bsx, int bsy, int bsz, unsigned long long &mask) {
   const int A = G.nx * G.ny;
   int w = u;
   for (;;) {
+    if (SLAB && (w < G.zb * A || w >= G.ze * A)) {
+      mask |= kExit;
+      return -(w + 1);
+    }
     brick_bit(x, y, z, bsx, bsy, bsz, mask);
     const int s = (__ldg(&slots[w]) >> (UP ? 4 : 0)) & 15;
     if (s == kSelf) return w;
@@ -1506,7 +1504,7 @@ __device__ __forceinline__ unsigned events_group(
       if (lower != SPLIT) {
         if (!FROM_REF) atomicAdd(&cnt[(size_t)(1 + (blockIdx.x & (kCntRep - 1))) * kCntStride + C_LINKS], 1ull);
         int e;
-        if constexpr (CACHE) e = walk_track<SPLIT>(u, ux, uy, uz, slots, G, bsx, bsy, bsz, mask);
+        if constexpr (CACHE) e = walk_track<SPLIT, SLAB>(u, ux, uy, uz, slots, G, bsx, bsy, bsz, mask);
         else e = walk<SPLIT, FROM_REF, SLAB>(u, slots, ref, G);
         if (!SLAB || e >= 0) {
           best = e + off;
@@ -1704,16 +1702,86 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
   }
 }
 
+// The rules of k_events (g paths), 16 lanes per saddle, one walk per lane (a
+// lane per link slot): the kernel lasts about as long as the longest single
+// path instead of a thread's ~7 paths in sequence.  For launches with too few
+// saddles to hide the walks' dependent loads (a z-slab holds 1/p of them).
+// Same bits as k_events: the same walks, the same SoS pick, the same target.
+template <bool SPLIT, bool SLAB>
+__global__ void __launch_bounds__(256) k_events16(const float *__restrict__ h,
+                                                  const int32_t *__restrict__ sl, int n,
+                                                  const uint8_t *__restrict__ slots,
+                                                  const uint32_t *__restrict__ lm,
+                                                  const int32_t *__restrict__ ref_ext,
+                                                  uint32_t *marks, GridP G, Slabs S,
+                                                  int32_t *remote, unsigned long long *cnt,
+                                                  const int32_t *__restrict__ lpos = nullptr) {
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+  const int l16 = threadIdx.x & 15;
+  const unsigned gmask = 0xffffu << (threadIdx.x & 16);  // this 16-lane group
+  const bool active = k < n;
+  const int A = G.nx * G.ny, off = G.zoff * A, lo = G.zb * A, hi = G.ze * A;
+  int s = 0;
+  uint32_t todo = 0;
+  if (active) {
+    s = __ldg(&sl[k]) - off;  // local
+    const uint32_t m = saddle_lm(lm, lpos, k, s);
+    todo = SPLIT ? (m >> 16) : (m & 0xFFFFu);
+  }
+  int best = -1;
+  float bv = 0.0f;
+  const bool mine = l16 < kSlots && ((todo >> l16) & 1u);
+  if (mine) {
+    const int e = walk<SPLIT, false, SLAB>(s + slot_delta(l16, G), slots, nullptr, G);
+    if (!SLAB || e >= 0) {
+      best = e + off;
+      bv = h[e];
+    } else {
+      const int2 t = table_lookup(S, -e - 1 + off, A);
+      best = t.x;
+      bv = __int_as_float(t.y);
+    }
+  }
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) {
+    const int ob = __shfl_xor_sync(gmask, best, o);
+    const float ov = __shfl_xor_sync(gmask, bv, o);
+    bool take;
+    if (ob < 0) take = false;
+    else if (best < 0) take = true;
+    else if (!SPLIT) take = (bv < ov) || (bv == ov && best < ob);  // SoS max
+    else take = (ov < bv) || (ov == bv && ob < best);               // SoS min
+    if (take) { best = ob; bv = ov; }
+  }
+  unsigned hit = 0;
+  if (active && l16 == 0) {
+    const int want = __ldg(&ref_ext[k]);
+    if (best >= 0 && best != want) {
+      const int target = SPLIT ? want : best;
+      const int t = target - off;
+      if (!SLAB || (t >= lo && t < hi)) mark_vertex(marks, t, G);
+      else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = target;
+      hit = 1;
+    }
+  }
+  warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
+  warp_add(&cnt[C_LINKS], mine ? 1u : 0u);
+}
+
 // Tracking: a saddle whose cached result is still valid (no brick it depends
 // on changed since the cached pass) re-emits it; the others are listed for
 // k_events_cached.  One thread per saddle.
-template <bool SPLIT>
+// SLAB: saddle ids and targets are global (a target in another slab goes to
+// `remote`, as k_events)
+template <bool SPLIT, bool SLAB = false>
 __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict__ sl, int n,
                                                       EvCache EC, Track T, uint32_t *marks,
                                                       GridP G, int *todo, int *ntodo,
                                                       unsigned long long *cnt,
                                                       const int *__restrict__ idx = nullptr,
-                                                      const int *__restrict__ nidx = nullptr) {
+                                                      const int *__restrict__ nidx = nullptr,
+                                                      int32_t *remote = nullptr) {
+  const int A = G.nx * G.ny, off = SLAB ? G.zoff * A : 0;
   // idx: only the saddles idx[0 .. *nidx) (left by k_fclean); else all n
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   bool act = k < n;
@@ -1726,13 +1794,13 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
   if (act) {
     const uint16_t rnd = EC.rnd[k];
     const unsigned long long mask = EC.mask[k];  // zeroed when the cache started
-    valid = rnd != 0 && !(mask & kFar);
+    valid = rnd != 0 && !(mask & kFar) && (!(mask & kExit) || rnd >= T.tab_round);
     if (valid) {
-      const int s = sl[k];
+      const int s = sl[k] - off;
       const int yz = div_nx(s, G), sz = div_ny(yz, G), sx = s - yz * G.nx, sy = yz - sz * G.ny;
       const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
       // the stamps of up to 4 bricks in flight per step (independent loads)
-      uint32_t m = (uint32_t)mask, ms = (uint32_t)(mask >> 32);
+      uint32_t m = (uint32_t)mask, ms = (uint32_t)(mask >> 32) & kSuperBits;
       while ((m | ms) && valid) {
         uint16_t st[8];
 #pragma unroll
@@ -1762,7 +1830,8 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
     if (valid) {
       const int t = EC.tgt[k];
       if (t >= 0) {
-        mark_vertex(marks, t, G);
+        if (!SLAB || (t - off >= G.zb * A && t - off < G.ze * A)) mark_vertex(marks, t - off, G);
+        else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = t;
         hit = 1;
       }
     }
@@ -1797,7 +1866,7 @@ __global__ void __launch_bounds__(256) k_events_check(const int32_t *__restrict_
 // k_events, recording the bricks the result depends on: the saddle's closed
 // star (its link masks come from those values) and every vertex of every walk
 // (a slot change anywhere on a path can move its root).
-template <bool SPLIT>
+template <bool SPLIT, bool SLAB = false>
 __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__ h,
                                                        const int32_t *__restrict__ sl,
                                                        const int *__restrict__ todo,
@@ -1808,7 +1877,9 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
                                                        GridP G, EvCache EC, Track T,
                                                        unsigned long long *cnt,
                                                        const int *__restrict__ todo2 = nullptr,
-                                                       const int *__restrict__ ntodo2 = nullptr) {
+                                                       const int *__restrict__ ntodo2 = nullptr,
+                                                       Slabs S = Slabs{nullptr, 1, nullptr},
+                                                       int32_t *remote = nullptr) {
   __shared__ int soff[16], sdel[16];  // linear offset; packed (dx+1, dy+1, dz+1)
   if (threadIdx.x < 16) {
     const int q = threadIdx.x;
@@ -1835,15 +1906,16 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
     // 16 lanes per saddle, one walk per lane, for the shortest critical path
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
     const bool active = g < n;
-    hit = events_group<SPLIT, false, true, false>(active ? todo[g] : 0, active, h, sl, slots, lm,
-                                                  nullptr, ref_ext, marks, G,
-                                                  Slabs{nullptr, 1, nullptr}, nullptr, EC, T, cnt);
+    hit = events_group<SPLIT, false, true, SLAB>(active ? todo[g] : 0, active, h, sl, slots, lm,
+                                                 nullptr, ref_ext, marks, G, S, remote, EC, T,
+                                                 cnt);
     warp_add(&cnt[C_N1 + 4 + (SPLIT ? 1 : 0)], hit);
     return;
   }
+  const int A = G.nx * G.ny, off = SLAB ? G.zoff * A : 0, lo = G.zb * A, hi = G.ze * A;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
     const int k = todo[g];
-    const int s = __ldg(&sl[k]);
+    const int s = __ldg(&sl[k]) - off;
     const int yz = div_nx(s, G), sz = div_ny(yz, G);
     const int sx = s - yz * G.nx, sy = yz - sz * G.ny;
     const int bsx = sx / BX, bsy = sy / BY, bsz = sz / BZ;
@@ -1880,11 +1952,16 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
 #endif
       int sv[2];
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
-        sv[j] = ((runm >> j) & 1u) ? (__ldg(&slots[w[j]]) >> (SPLIT ? 4 : 0)) & 15 : kSelf;
+      for (int j = 0; j < 2; ++j) {
+        sv[j] = kSelf;
+        if ((runm >> j) & 1u) {
+          if (!SLAB || (w[j] >= lo && w[j] < hi)) sv[j] = (__ldg(&slots[w[j]]) >> (SPLIT ? 4 : 0)) & 15;
+          else sv[j] = -1;  // the exit into a neighbour's slab
+        }
+      }
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        if (sv[j] != kSelf) {
+        if (sv[j] >= 0 && sv[j] != kSelf) {
           const int p = sdel[sv[j]];
           w[j] += soff[sv[j]];
           x[j] += (p & 3) - 1;
@@ -1895,8 +1972,17 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
         }
         if (!((runm >> j) & 1u)) continue;
         runm &= ~(1u << j);
-        const int lab = w[j];
-        const float val = h[lab];
+        int lab;
+        float val;
+        if (!SLAB || sv[j] >= 0) {
+          lab = w[j] + off;
+          val = h[w[j]];
+        } else {  // completed from the boundary tables
+          const int2 t = table_lookup(S, w[j] + off, A);
+          lab = t.x;
+          val = __int_as_float(t.y);
+          mask |= kExit;
+        }
         bool take;
         if (best < 0) take = true;
         else if (!SPLIT) take = (bv < val) || (bv == val && best < lab);  // SoS max
@@ -1911,7 +1997,8 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
     EC.mask[k] = mask;
     EC.tgt[k] = target;
     if (target >= 0) {
-      mark_vertex(marks, target, G);
+      if (!SLAB || (target - off >= lo && target - off < hi)) mark_vertex(marks, target - off, G);
+      else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = target;
       ++hit;  // a lane may recompute several saddles (grid-stride)
     }
   }
@@ -2114,6 +2201,36 @@ __device__ __forceinline__ void cta_append(bool need, int k, int *todo, int *nto
   __syncthreads();  // wcnt / wbase are reused by the next call
 }
 
+// CTA-aggregated append to a list counted by *n (64-bit): returns this
+// thread's position if `need`, else -1; one atomic per CTA.  Every thread of
+// the block calls it (it synchronises the block).
+__device__ __forceinline__ long long cta_slot(bool need, unsigned long long *n) {
+  __shared__ int wcnt[32];
+  __shared__ unsigned long long wbase[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, need);
+  if (lane == 0) wcnt[wid] = __popc(m);
+  __syncthreads();
+  if (wid == 0) {
+    const int c = lane < nw ? wcnt[lane] : 0;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, inc, 31);
+    unsigned long long base = 0;
+    if (lane == 0 && tot) base = atomicAdd(n, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane < nw) wbase[lane] = base + (unsigned long long)(inc - c);
+  }
+  __syncthreads();
+  const long long r = need ? (long long)(wbase[wid] + __popc(m & ((1u << lane) - 1u))) : -1;
+  __syncthreads();  // wcnt / wbase are reused by the next call
+  return r;
+}
+
 // Per pass: a saddle whose link partition is f's and whose f-walk tiles are
 // all clean takes X = X_f (R5 / R6 without walks); the others are listed in
 // todo for the walk kernels.  idx: only the saddles idx[0 .. *nidx) (those
@@ -2218,13 +2335,129 @@ __global__ void __launch_bounds__(256) k_fclean(const float *__restrict__ g,
 }
 
 // ------------------------------------------------ sharded helpers (z-slabs)
+// The g boundary tables of a pass after the first, both directions in one
+// launch (4A entries: dir, side, xy): each entry of this rank is recomputed,
+// and one that differs from the replicated table's is written there and
+// listed {position in the table pair [dn | up], label, value bits} for the
+// other ranks (sparse all-gather); the tables stay equal on every rank.
+// CACHE (the C3 cache is on): an entry whose walk visited no brick stamped
+// since it was walked (value or slot change, kernels.cuh Track) is unchanged
+// and not walked again; the exit into a neighbour's slab is a position, not
+// data, so every entry is cacheable (unless its path left the superbrick
+// neighbourhood: kFar).  brnd / bmask: the round and bricks of each entry.
+template <bool CACHE>
+__global__ void k_boundary_delta(const float *__restrict__ h, const uint8_t *__restrict__ slots,
+                                 GridP G, int rank, int p, int2 *tab, int4 *upd,
+                                 unsigned long long *nupd, Track T = Track{},
+                                 uint16_t *brnd = nullptr, unsigned long long *bmask = nullptr) {
+  const int A = G.nx * G.ny;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool chg = false;
+  int pos = 0;
+  int2 val = make_int2(0, 0);
+  if (i < 4 * A) {
+    const int dir = i >= 2 * A, j = i - dir * 2 * A, side = j >= A, xy = j - side * A;
+    const int lo = G.zb * A, hi = G.ze * A, sh = dir ? 4 : 0;
+    int y = xy / G.nx, x = xy - y * G.nx, z = side ? G.ze - 1 : G.zb;
+    const int bsx = x / BX, bsy = y / BY, bsz = z / BZ;
+    bool walk = true;
+    if (CACHE) {
+      const uint16_t r0 = brnd[i];
+      const unsigned long long m0 = bmask[i];
+      if (r0 != 0 && !(m0 & kFar)) {
+        walk = false;
+        uint32_t m = (uint32_t)m0, ms = (uint32_t)(m0 >> 32);
+        while ((m | ms) && !walk) {
+          uint16_t a, b;
+          if (m) {
+            const int q = __ffs(m) - 1;
+            m &= m - 1;
+            const int nb = (bsx + q % 3 - 1) + T.nbx * ((bsy + (q / 3) % 3 - 1) + T.nby * (bsz + q / 9 - 1));
+            a = T.bval[nb];
+            b = T.bslot[nb];
+          } else {
+            const int q = __ffs(ms) - 1;
+            ms &= ms - 1;
+            const int nb = (bsx / SB + q % 3 - 1) +
+                           T.nsx * ((bsy / SB + (q / 3) % 3 - 1) + T.nsy * (bsz / SB + q / 9 - 1));
+            a = T.sbval[nb];
+            b = T.sbslot[nb];
+          }
+          if (a > r0 || b > r0) walk = true;
+        }
+      }
+    }
+    if (walk) {
+      unsigned long long mask = 0;
+      int w = (side ? G.ze - 1 : G.zb) * A + xy, e;
+      for (;;) {  // walk(): the steepest path of g inside the slab
+        if (w < lo || w >= hi) {
+          e = -(w + 1);
+          break;
+        }
+        if (CACHE) brick_bit(x, y, z, bsx, bsy, bsz, mask);
+        const int sl = (__ldg(&slots[w]) >> sh) & 15;
+        if (sl == kSelf) {
+          e = w;
+          break;
+        }
+        const int b = slot_bits(sl), sg1 = slot_sign(sl);
+        x += sg1 * (b & 1);
+        y += sg1 * ((b >> 1) & 1);
+        z += sg1 * (b >> 2);
+        w += sg1 * ((b & 1) + ((b >> 1) & 1) * G.nx + (b >> 2) * A);
+      }
+      if (CACHE) {
+        brnd[i] = (uint16_t)T.round;
+        bmask[i] = mask;
+      }
+      const int off = G.zoff * A;
+      val = e >= 0 ? make_int2(e + off, __float_as_int(h[e])) : make_int2(-(-e - 1 + off) - 1, 0);
+      pos = dir * 2 * p * A + (2 * rank + side) * A + xy;
+      const int2 old = tab[pos];
+      chg = old.x != val.x || old.y != val.y;
+      if (chg) tab[pos] = val;
+    }
+  }
+  // warp-aggregated append
+  const long long q = cta_slot(chg, nupd);  // (a dense pass changes most entries)
+  if (q >= 0) upd[q] = make_int4(pos, val.x, val.y, 0);
+}
+// A slab's ghost planes after the halo refresh: a vertex whose value changed
+// (the neighbour's edit of its boundary plane) stamps its brick as an edit of
+// this pass does (round + 1), so the C3 cache sees a saddle star or a walk
+// that reads it change; prev keeps the planes' last values.
+__global__ void k_ghost_stamp(const float *__restrict__ g, float *prev, GridP G, Track T) {
+  const int A = G.nx * G.ny;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * A) return;
+  const int side = i >= A, xy = i - side * A, z = side ? G.nz - 1 : 0;
+  const float v = g[(size_t)z * A + xy];
+  if (__float_as_uint(v) == __float_as_uint(prev[i])) return;
+  prev[i] = v;
+  const int y = xy / G.nx, x = xy - y * G.nx;
+  stamp(T.bval, T.sbval, T, x / BX, y / BY, z / BZ, (uint16_t)(T.round + 1));
+}
+
+// gathered table updates (position < 0: padding)
+__global__ void k_apply_tab(const int4 *__restrict__ upd, int n, int2 *tab) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int4 u = upd[k];
+  if (u.x >= 0) tab[u.x] = make_int2(u.y, u.z);
+}
+
+
 // R4 with the replicated saddle values gS (uint32 bit patterns, S order):
 // the owner of S[k] checks the pair (S[k], S[k+1]).
+// own: only the positions k of the pairs whose S[k] the slab owns (nown of them)
 __global__ void k_saddle_order_slab(const uint32_t *__restrict__ gS,
                                     const int32_t *__restrict__ S, int nS, uint32_t *marks,
-                                    GridP G, unsigned long long *cnt, int ci = C_N1 + 3) {
+                                    GridP G, unsigned long long *cnt, int ci = C_N1 + 3,
+                                    const int32_t *__restrict__ own = nullptr, int nown = 0) {
   unsigned n4 = 0;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = own ? (j < nown ? __ldg(&own[j]) : nS) : j;
   const int A = G.nx * G.ny, off = G.zoff * A;
   if (k + 1 < nS) {
     const int a = S[k] - off;
@@ -2238,6 +2471,16 @@ __global__ void k_saddle_order_slab(const uint32_t *__restrict__ gS,
   }
   warp_add(&cnt[ci], n4);
 }
+
+// S[k] lies in the owned planes [lo, hi) (global ids): R4's pairs of a slab
+struct OwnedInS {
+  const int32_t *S;
+  int lo, hi;
+  __device__ __forceinline__ bool operator()(int k) const {
+    const int a = S[k];
+    return a >= lo && a < hi;
+  }
+};
 
 // gS[k] = bits of g at S[k] for owned saddles, 0 elsewhere (max-all-reduced)
 __global__ void k_fill_gS(const float *__restrict__ g, const int32_t *__restrict__ S, int nS,
@@ -2270,6 +2513,27 @@ __global__ void k_local_pos(const int32_t *__restrict__ S, int nS, int32_t *pos,
   const int A = G.nx * G.ny, a = S[k] - G.zoff * A;
   if (a >= G.zb * A && a < G.ze * A) pos[a] = k;
 }
+// The owned entries of the replicated gS (positions own[0 .. n)) that the
+// stencil changed this pass, listed (position, value bits) for the sparse
+// all-gather; prev keeps the last listed values.  A separate pass over the
+// slab's ~nS / p entries: appending from inside the dense stencil made it
+// spill (ptxas: 500 bytes of spill stores) and run 1.6x longer.
+__global__ void k_gs_diff(const int32_t *__restrict__ own, int n, const uint32_t *__restrict__ gS,
+                          uint32_t *prev, int2 *upd, unsigned long long *nupd) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int k = 0;
+  uint32_t v = 0;
+  bool chg = false;
+  if (j < n) {
+    k = __ldg(&own[j]);
+    v = gS[k];
+    chg = prev[k] != v;
+    if (chg) prev[k] = v;
+  }
+  const long long q = cta_slot(chg, nupd);
+  if (q >= 0) upd[q] = make_int2(k, (int)v);
+}
+
 // gathered (position, value bits) updates into the replicated gS (pos < 0: padding)
 __global__ void k_apply_gs(const int2 *__restrict__ upd, int n, uint32_t *gS) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;

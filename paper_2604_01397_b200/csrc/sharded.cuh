@@ -3,16 +3,25 @@
 // Each rank owns the planes [z0, z0 + nzl) of the field and keeps one ghost
 // plane on each side (local planes 0 and nzl + 1; NaN at the global faces).
 // Per round (Alg. 1), bit-exact with the single-GPU call:
-//   1. stencil R1-R3 on the owned planes (needs the ghost g planes);
-//   2. C2 (R4) on the replicated saddle values gS: every rank fills the
-//      entries it owns, a max-all-reduce over the uint32 bit patterns gives
-//      every rank all values (exactly one non-zero contribution per entry);
-//   3. C3 (R5/R6): label walks inside the slab; a path that leaves the slab
-//      is completed from the gathered boundary table (§ k_boundary_walks);
-//      targets owned by another rank travel in an all-gathered list;
-//   4. marks that fall in a ghost plane go back to the owning neighbour;
-//   5. the owners count and edit; the 8 round counters are all-reduced;
-//   6. the new g boundary planes refresh the neighbours' ghost planes.
+//   1. stencil R1-R3 on the owned planes (needs the ghost g planes): the key
+//      stencils of exactz_correct (TMA-staged dense pass, list passes once
+//      the marks are sparse), which also keep the owned entries of the
+//      replicated saddle values gS and list the changed ones;
+//   2. the g boundary tables (every vertex of the first / last owned plane:
+//      the terminus of its steepest path inside the slab) recomputed, the
+//      changed entries listed;
+//   3. exchange A: one count all-reduce sizes two sparse all-gathers, the
+//      changed gS entries and the changed table entries (the whole tables in
+//      the first pass, or when more than half of a rank's entries changed);
+//   4. C2 (R4) on the pairs whose lower saddle the rank owns;
+//   5. C3 (R5/R6): label walks inside the slab; a path that leaves the slab
+//      is completed from the gathered tables (table_lookup); once the marks
+//      are sparse at brick scale, the brick-stamp cache of exactz_correct
+//      re-emits the results whose walks stayed inside the slab;
+//   6. exchange B: targets owned by another rank (sparse all-gather);
+//   7. marks that fall in a ghost plane go back to the owning neighbour;
+//   8. the owners count and edit; the round counters are all-reduced;
+//   9. the new g boundary planes refresh the neighbours' ghost planes.
 // The paper's distributed protocol exchanges ghost layers and
 // uses "a consistent rule ... prioritizing smaller scalar modifications";
 // here owners compute every edit and marks are ORed, so no tie rule is
@@ -20,7 +29,8 @@
 //
 // Transport: NCCL (one rank per process/GPU, exactz_correct_sharded) or a
 // loopback that runs every rank of the decomposition in one process on one
-// GPU (exactz_correct_slabs), used to test the decomposition on one device.
+// GPU (exactz_correct_slabs), used to test the decomposition on one device;
+// its collectives are single kernels over the ranks' buffers.
 #pragma once
 #include <nccl.h>
 
@@ -64,6 +74,54 @@ __global__ void k_max_u32(uint32_t *acc, const uint32_t *src, size_t n) {
   if (k < n) acc[k] = src[k] > acc[k] ? src[k] : acc[k];
 }
 
+// Loopback collectives as single launches (up to kLoopMax ranks): the
+// ranks' buffers are all on this GPU, so a collective is one kernel over its
+// segments instead of p or p^2 stream-ordered copies, whose launch costs
+// would otherwise dominate the loopback's per-pass time (an artifact: with
+// NCCL each rank issues one collective).
+constexpr int kLoopMax = 16;
+struct LoopPtrs {
+  const char *a[kLoopMax];
+};
+struct LoopMPtrs {
+  char *a[kLoopMax];
+};
+// block-strided copy of one segment (16-byte vectors when everything is aligned)
+__device__ __forceinline__ void seg_copy(char *dst, const char *src, size_t bytes) {
+  if (dst == src) return;
+  const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+  if ((((uintptr_t)dst | (uintptr_t)src | bytes) & 15) == 0) {
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    for (size_t k = t0; k < bytes / 16; k += st) d4[k] = s4[k];
+  } else {
+    for (size_t k = t0; k < bytes; k += st) dst[k] = src[k];
+  }
+}
+// segment y = l * p + r: recv[l] + r * bytes <- send[r]
+__global__ void k_loop_allgather(LoopPtrs send, LoopMPtrs recv, int p, size_t bytes) {
+  const int l = blockIdx.y / p, r = blockIdx.y - l * p;
+  seg_copy(recv.a[l] + r * bytes, send.a[r], bytes);
+}
+// segment y = 2 r + d: d = 0: hi_recv[r - 1] <- lo_send[r]; d = 1: lo_recv[r + 1] <- hi_send[r]
+__global__ void k_loop_halo(LoopPtrs lo_send, LoopPtrs hi_send, LoopMPtrs lo_recv,
+                            LoopMPtrs hi_recv, int p, size_t bytes) {
+  const int r = blockIdx.y >> 1, d = blockIdx.y & 1;
+  if (d == 0 && r > 0) seg_copy(hi_recv.a[r - 1], lo_send.a[r], bytes);
+  if (d == 1 && r + 1 < p) seg_copy(lo_recv.a[r + 1], hi_send.a[r], bytes);
+}
+template <class T, bool MAX>
+__global__ void k_loop_reduce(LoopMPtrs buf, int p, size_t n) {
+  const size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  T v = reinterpret_cast<T *>(buf.a[0])[k];
+  for (int l = 1; l < p; ++l) {
+    const T x = reinterpret_cast<T *>(buf.a[l])[k];
+    v = MAX ? (x > v ? x : v) : v + x;
+  }
+  for (int l = 0; l < p; ++l) reinterpret_cast<T *>(buf.a[l])[k] = v;
+}
+
 struct LoopTransport : Transport {
   int p;
   cudaStream_t s;
@@ -72,9 +130,31 @@ struct LoopTransport : Transport {
   int nranks() const override { return p; }
   int nlocal() const override { return p; }
   int rank_of(int l) const override { return l; }
+  template <class V>
+  static LoopPtrs cptrs(const V &v) {
+    LoopPtrs q{};
+    for (size_t k = 0; k < v.size(); ++k) q.a[k] = (const char *)v[k];
+    return q;
+  }
+  template <class V>
+  static LoopMPtrs mptrs(const V &v) {
+    LoopMPtrs q{};
+    for (size_t k = 0; k < v.size(); ++k) q.a[k] = (char *)v[k];
+    return q;
+  }
+  static unsigned seg_blocks(size_t bytes) {
+    return (unsigned)std::min<size_t>(std::max<size_t>((bytes / 16 + 255) / 256, 1), 256);
+  }
   void halo(const std::vector<const void *> &lo_send, const std::vector<const void *> &hi_send,
             const std::vector<void *> &lo_recv, const std::vector<void *> &hi_recv,
             size_t bytes) override {
+    if (p < 2 || !bytes) return;
+    if (p <= kLoopMax) {
+      k_loop_halo<<<dim3(seg_blocks(bytes), 2 * p), 256, 0, s>>>(
+          cptrs(lo_send), cptrs(hi_send), mptrs(lo_recv), mptrs(hi_recv), p, bytes);
+      CK(cudaGetLastError());
+      return;
+    }
     for (int r = 0; r < p; ++r) {
       if (r > 0) CK(cudaMemcpyAsync(hi_recv[r - 1], lo_send[r], bytes, cudaMemcpyDefault, s));
       if (r + 1 < p) CK(cudaMemcpyAsync(lo_recv[r + 1], hi_send[r], bytes, cudaMemcpyDefault, s));
@@ -82,18 +162,38 @@ struct LoopTransport : Transport {
   }
   void allgather(const std::vector<const void *> &send, const std::vector<void *> &recv,
                  size_t bytes) override {
+    if (!bytes) return;
+    if (p <= kLoopMax) {
+      k_loop_allgather<<<dim3(seg_blocks(bytes), p * p), 256, 0, s>>>(cptrs(send), mptrs(recv), p,
+                                                                      bytes);
+      CK(cudaGetLastError());
+      return;
+    }
     for (int l = 0; l < p; ++l)
       for (int r = 0; r < p; ++r)
-        CK(cudaMemcpyAsync((char *)recv[l] + r * bytes, send[r], bytes, cudaMemcpyDefault, s));
+        if ((const char *)recv[l] + r * bytes != send[r])  // (in place: nothing to copy)
+          CK(cudaMemcpyAsync((char *)recv[l] + r * bytes, send[r], bytes, cudaMemcpyDefault, s));
   }
   void allreduce_sum_u64(const std::vector<unsigned long long *> &buf, size_t n) override {
+    if (p < 2 || !n) return;
+    if (p <= kLoopMax) {
+      k_loop_reduce<unsigned long long, false><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+          mptrs(buf), p, n);
+      CK(cudaGetLastError());
+      return;
+    }
     for (int l = 1; l < p; ++l)
       k_sum_u64<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(buf[0], buf[l], (int)n);
     CK(cudaGetLastError());
     for (int l = 1; l < p; ++l) CK(cudaMemcpyAsync(buf[l], buf[0], n * 8, cudaMemcpyDefault, s));
   }
   void allreduce_max_u32(const std::vector<uint32_t *> &buf, size_t n) override {
-    if (!n) return;
+    if (p < 2 || !n) return;
+    if (p <= kLoopMax) {
+      k_loop_reduce<uint32_t, true><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(mptrs(buf), p, n);
+      CK(cudaGetLastError());
+      return;
+    }
     for (int l = 1; l < p; ++l)
       k_max_u32<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(buf[0], buf[l], n);
     CK(cudaGetLastError());
@@ -158,7 +258,13 @@ struct Slab {
   GridP G{};
   dim3 sgrid;
   int zc = 1;
-  bool fast = false;  // every owned lo >= 0: k_stencil_fast
+  bool fast = false;  // every lo >= 0 (all ranks): k_stencil_fast
+  bool keyed = false; // the call's value range fits exact SoS keys: the key stencils
+  bool tma = false;   // k_stencil_key2 stages planes by TMA (tmap over this slab's g)
+  CUtensorMap tmap{};
+  uint32_t *kmm = nullptr;  // ~bits(lo_min), bits(g_max) of this rank, max-reduced
+  int32_t *own = nullptr;   // positions k in S whose S[k] this slab owns (R4 pairs)
+  int nown = 0;
   float *f = nullptr, *g = nullptr;
   uint32_t *ref = nullptr, *marks = nullptr, *ghost_lo = nullptr, *ghost_hi = nullptr;
   uint8_t *slots = nullptr, *c = nullptr;
@@ -166,15 +272,19 @@ struct Slab {
   uint64_t *keys = nullptr, *allkeys = nullptr, *sorted = nullptr;
   int32_t *S = nullptr, *J = nullptr, *P = nullptr, *m1 = nullptr, *M1 = nullptr;
   int nJ = 0, nP = 0;
-  int2 *tdn = nullptr, *tup = nullptr;  // gathered boundary tables (2 p A)
+  int2 *tdn = nullptr, *tup = nullptr;  // gathered boundary tables (2 p A each, contiguous)
+  int4 *tupd = nullptr, *alltupd = nullptr;  // changed table entries: this rank's / gathered
+  size_t alltupd_cap = 0;
   uint32_t *gS = nullptr;
   uint64_t *cpkeys = nullptr;
   int32_t *CP = nullptr;  // reformulation: all critical points, replicated
   uint32_t *gC = nullptr;
   int32_t *remote = nullptr, *allremote = nullptr;
+  size_t allremote_cap = 0;  // grown on demand (geometric)
   // sparse exchange of the replicated gS: positions in S of the owned
   // saddles (local index), this round's changed entries, all ranks' lists
   int32_t *posS = nullptr;
+  uint32_t *gSprev = nullptr;  // the owned entries as last listed (k_gs_diff)
   int2 *upd = nullptr, *allupd = nullptr;
   unsigned long long *cnt = nullptr, *hcnt = nullptr;  // device counters / host mirror
   unsigned long long *nrem = nullptr;                    // per-rank remote counts (p)
@@ -184,6 +294,15 @@ struct Slab {
   uint32_t *act[2] = {nullptr, nullptr}, *edited = nullptr;
   int32_t *list = nullptr;
   int *nlist = nullptr;
+  // the C3 cache (brick stamps, as exactz_correct's Tracking) over the local
+  // buffer; results whose walks leave the slab are never reused (kFar)
+  int nbx = 0, nby = 0, nbz = 0, nsx = 0, nsy = 0, nsz = 0;
+  uint16_t *bval = nullptr, *bslot = nullptr, *sbval = nullptr, *sbslot = nullptr;
+  EvCache ecJ{}, ecP{};
+  int *todo = nullptr, *todoP = nullptr, *ntodo = nullptr;
+  float *ghost_prev = nullptr;         // the ghost planes' values as last stamped
+  uint16_t *brnd = nullptr;            // boundary-table entries: round and bricks of the
+  unsigned long long *bmask = nullptr; // last walk (k_boundary_delta<true>)
   size_t plane() const { return (size_t)G.nx * G.ny; }
   size_t words_per_plane() const { return (size_t)G.ny * G.W; }
 };
@@ -200,6 +319,10 @@ struct ShardedRun {
   float xi, delta;
   uint32_t flags;
   bool act_on = false, ready = false;  // vertex activity started / act[cur] valid
+  bool cache_on = false;               // the C3 cache started
+  int rnd = 0;                         // pass number (16-bit stamps of the cache)
+  int tab_round = 0;                   // last pass in which a g boundary-table entry changed
+  bool tables_ready = false;           // the g boundary tables hold a previous pass's
   int cur = 0;
 
   ShardedRun(Transport &t, cudaStream_t st, Arena &a, std::vector<Slab> &slabs, int nx_, int ny_,
@@ -241,6 +364,48 @@ struct ShardedRun {
     });
     act_on = true;
   }
+  void start_cache() {
+    each([&](Slab &x) {
+      x.nbx = (x.G.nx + BX - 1) / BX;
+      x.nby = (x.G.ny + BY - 1) / BY;
+      x.nbz = (x.G.nz + BZ - 1) / BZ;
+      x.nsx = (x.nbx + SB - 1) / SB;
+      x.nsy = (x.nby + SB - 1) / SB;
+      x.nsz = (x.nbz + SB - 1) / SB;
+      const size_t nb = (size_t)x.nbx * x.nby * x.nbz, nsb = (size_t)x.nsx * x.nsy * x.nsz;
+      uint16_t *st = A.get<uint16_t>(2 * (nb + nsb));
+      CK(cudaMemsetAsync(st, 0, 2 * (nb + nsb) * 2, s));
+      x.bval = st;
+      x.bslot = st + nb;
+      x.sbval = st + 2 * nb;
+      x.sbslot = x.sbval + nsb;
+      auto cache = [&](int n) {
+        EvCache e{};
+        const size_t m = n > 0 ? (size_t)n : 1;
+        e.rnd = A.get<uint16_t>(m);
+        e.mask = A.get<unsigned long long>(m);
+        e.tgt = A.get<int32_t>(m);
+        CK(cudaMemsetAsync(e.rnd, 0, m * 2, s));
+        CK(cudaMemsetAsync(e.mask, 0, m * 8, s));
+        return e;
+      };
+      x.ecJ = cache(x.nJ);
+      x.ecP = cache(x.nP);
+      const size_t A4 = 4 * x.plane();
+      x.ghost_prev = A.get<float>(2 * x.plane());
+      CK(cudaMemcpyAsync(x.ghost_prev, x.g, x.plane() * 4, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(x.ghost_prev + x.plane(), x.g + (size_t)(x.G.nz - 1) * x.plane(),
+                         x.plane() * 4, cudaMemcpyDeviceToDevice, s));
+      x.brnd = A.get<uint16_t>(A4);
+      x.bmask = A.get<unsigned long long>(A4);
+      CK(cudaMemsetAsync(x.brnd, 0, A4 * 2, s));
+      x.todo = A.get<int>(std::max(x.nJ, 1));
+      x.todoP = A.get<int>(std::max(x.nP, 1));
+      x.ntodo = A.get<int>(2);
+    });
+    cache_on = true;
+  }
+
   // the neighbours' edits of their boundary planes into the ghost planes of
   // `edited` (stars that cross the slab border)
   void halo_edited() {
@@ -299,7 +464,14 @@ struct ShardedRun {
       G.gnz = nz;
       G.zb = 1;
       G.ze = x.nzl + 1;
-      x.zc = std::min(32, std::max(1, x.nzl));
+      {  // z chunk per stencil CTA, as exactz_correct: enough CTAs for several
+         // waves on 148 SMs (a slab of 64 planes in chunks of 32 left the key
+         // stencil 2.3 waves, 30 % lost to the tail), >= 8 planes per chunk
+        const int64_t cols = (int64_t)((nx + TX - 1) / TX) * ((ny + TY - 1) / TY), want = 148 * 24;
+        const int64_t z = cols >= want ? x.nzl : (x.nzl * cols + want - 1) / want;
+        x.zc = (int)std::min<int64_t>(std::max<int64_t>(z, 8), 64);
+        x.zc = std::max(1, std::min(x.zc, x.nzl));
+      }
       x.sgrid = dim3((unsigned)((nx + TX - 1) / TX), (unsigned)((ny + TY - 1) / TY),
                      (unsigned)((x.nzl + x.zc - 1) / x.zc));
       const size_t P = x.plane(), Vl = (size_t)G.V;
@@ -314,11 +486,17 @@ struct ShardedRun {
       x.ghost_hi = A.get<uint32_t>(x.words_per_plane());
       x.cnt = A.get<unsigned long long>(C_NALLOC);
       CK(cudaMallocHost(&x.hcnt, C_NCOUNTERS * 8));
-      x.nrem = A.get<unsigned long long>(2 * p);
+      x.nrem = A.get<unsigned long long>(3 * p);
       x.keys = A.get<uint64_t>(x.nzl * P);
       if (reform) x.cpkeys = A.get<uint64_t>(x.nzl * P);
-      x.tdn = A.get<int2>(2 * p * P);
-      x.tup = A.get<int2>(2 * p * P);
+      // the table pair [dn | up] (k_boundary_delta's positions), this rank's
+      // changed entries, and the gathered changes (at most A / 2 per rank:
+      // beyond that the whole chunks travel)
+      x.tdn = A.get<int2>(4 * p * P);
+      x.tup = x.tdn + 2 * p * P;
+      x.tupd = A.get<int4>(4 * P);
+      x.alltupd = A.get<int4>(p * (P / 2 + 1));
+      x.alltupd_cap = p * (P / 2 + 1);
       // owned planes from the caller; ghost planes NaN until the halo exchange
       CK(cudaMemsetAsync(x.f, 0xff, Vl * 4, s));
       CK(cudaMemsetAsync(x.g, 0xff, Vl * 4, s));
@@ -336,6 +514,22 @@ struct ShardedRun {
       k_validate<<<blocks_for(x.nzl * P, 256), 256, 0, s>>>(x.f + P, x.g + P, x.nzl * P, xi, x.cnt);
     });
     CK(cudaGetLastError());
+    // the value range of the call (the key stencils' applicability, as
+    // exactz_correct decides it from the whole field): max over the ranks
+    {
+      std::vector<uint32_t *> km;
+      each([&](Slab &x) {
+        x.kmm = A.get<uint32_t>(2);
+        CK(cudaMemcpyAsync(x.kmm, reinterpret_cast<const uint32_t *>(x.cnt + C_KEYMIN), 4,
+                           cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(x.kmm + 1, reinterpret_cast<const uint32_t *>(x.cnt + C_KEYMAX), 4,
+                           cudaMemcpyDeviceToDevice, s));
+        km.push_back(x.kmm);
+      });
+      T.allreduce_max_u32(km, 2);
+    }
+    uint32_t hk[2] = {0, 0};
+    CK(cudaMemcpyAsync(hk, sl[0].kmm, sizeof(hk), cudaMemcpyDeviceToHost, s));
     // C_NEG too: every slab must make the single-GPU call's fast/general
     // stencil choice, which depends on the whole field (the halo planes of a
     // slab hold a neighbour's values).  The other counters are zero here.
@@ -349,7 +543,16 @@ struct ShardedRun {
       set_err("validate", "|f - g| > eps for some vertex");
       throw Error{EXACTZ_EBOUND};
     }
-    each([&](Slab &x) { x.fast = x.hcnt[C_NEG] == 0 && !(flags & 0x800u); });
+    each([&](Slab &x) {
+      x.fast = x.hcnt[C_NEG] == 0 && !(flags & 0x800u);
+      // exact SoS keys (stencil_key.cuh), as exactz_correct (debug 0x2000: off)
+      const uint32_t lo_min = ~hk[0], g_max = hk[1];
+      x.keyed = x.fast && !(flags & 0x2000u) && lo_min >= kKeyLoMinBits &&
+                g_max < kKeyHiMaxBits && g_max >= lo_min && g_max - lo_min < kKeySpan;
+      for (int q = 0; q < kSlots; ++q) x.G.kc[q] = (uint32_t)q - 16u * lo_min;
+      // (debug 0x8000: thread-staged planes)
+      x.tma = x.keyed && !(flags & 0x8000u) && encode_plane_map(&x.tmap, x.g, nx, ny, x.G.nz);
+    });
     // O7 reference of f on the owned planes
     zero_counters();
     each([&](Slab &x) {
@@ -398,7 +601,8 @@ struct ShardedRun {
       CK(cub::DeviceRadixSort::SortKeys(tmp, tb, x.allkeys, x.sorted, (int)(slot * p), 0, 64, s));
       if (nS) k_keys_to_ids<<<(nS + 255) / 256, 256, 0, s>>>(x.sorted, x.S, nS);
       x.gS = A.get<uint32_t>(std::max(nS, 1));
-      x.remote = A.get<int32_t>(std::max(nS, 1));
+      // (a walk target per join and per split saddle the slab owns)
+      x.remote = A.get<int32_t>(2 * (size_t)std::max(nS, 1));
       x.posS = A.get<int32_t>(x.G.V);
       CK(cudaMemsetAsync(x.posS, 0xff, (size_t)x.G.V * 4, s));
       if (nS) k_local_pos<<<(nS + 255) / 256, 256, 0, s>>>(x.S, nS, x.posS, x.G);
@@ -408,19 +612,27 @@ struct ShardedRun {
       const int lo = x.G.zb * (int)x.plane(), n = x.nzl * (int)x.plane();
       x.J = A.get<int32_t>(std::max<int64_t>(counts[x.rank], 1));
       x.P = A.get<int32_t>(std::max<int64_t>(counts[x.rank], 1));
-      int *nsel = A.get<int>(2);
+      int *nsel = A.get<int>(3);
       cub::CountingInputIterator<int32_t> ids(lo);
-      size_t t2 = 0, t3 = 0;
+      // R4 pairs (S[k], S[k+1]) whose S[k] this slab owns: their positions k
+      x.own = A.get<int32_t>(std::max(nS, 1));
+      cub::CountingInputIterator<int32_t> ks(0);
+      const OwnedInS ow{x.S, x.z0 * (int)x.plane(), (x.z0 + x.nzl) * (int)x.plane()};
+      size_t t2 = 0, t3 = 0, t4 = 0;
       CK(cub::DeviceSelect::If(nullptr, t2, ids, x.J, nsel, n, IsJoin{x.ref}, s));
       CK(cub::DeviceSelect::If(nullptr, t3, ids, x.P, nsel + 1, n, IsSplit{x.ref}, s));
-      void *tmp2 = A.get<uint8_t>(std::max(t2, t3));
+      CK(cub::DeviceSelect::If(nullptr, t4, ks, x.own, nsel + 2, std::max(nS, 1), ow, s));
+      void *tmp2 = A.get<uint8_t>(std::max(std::max(t2, t3), t4));
       CK(cub::DeviceSelect::If(tmp2, t2, ids, x.J, nsel, n, IsJoin{x.ref}, s));
       CK(cub::DeviceSelect::If(tmp2, t3, ids, x.P, nsel + 1, n, IsSplit{x.ref}, s));
-      int h[2];
+      if (nS) CK(cub::DeviceSelect::If(tmp2, t4, ks, x.own, nsel + 2, nS, ow, s));
+      else CK(cudaMemsetAsync(nsel + 2, 0, sizeof(int), s));
+      int h[3];
       CK(cudaMemcpyAsync(h, nsel, sizeof(h), cudaMemcpyDeviceToHost, s));
       sync();
       x.nJ = h[0];
       x.nP = h[1];
+      x.nown = h[2];
       const int off = x.G.zoff * (int)x.plane();
       if (x.nJ) k_add_offset<<<(x.nJ + 255) / 256, 256, 0, s>>>(x.J, x.nJ, off);
       if (x.nP) k_add_offset<<<(x.nP + 255) / 256, 256, 0, s>>>(x.P, x.nP, off);
@@ -437,6 +649,10 @@ struct ShardedRun {
         b.push_back(x.gS);
       });
       T.allreduce_max_u32(b, nS);
+      each([&](Slab &x) {
+        x.gSprev = A.get<uint32_t>(nS);
+        CK(cudaMemcpyAsync(x.gSprev, x.gS, (size_t)nS * 4, cudaMemcpyDeviceToDevice, s));
+      });
     }
     if (reform) {
       gather_sorted(C_NCP, [](Slab &x) { return x.cpkeys; },
@@ -508,6 +724,15 @@ struct ShardedRun {
     CK(cudaGetLastError());
   }
 
+  // (the gathered table changes exceed A / 2 per rank only under debug 0x800000)
+  size_t x_alltupd_cap() const { return sl[0].alltupd_cap; }
+  void grow_alltupd(size_t n) {
+    each([&](Slab &x) {
+      x.alltupd = A.get<int4>(n);
+      x.alltupd_cap = n;
+    });
+  }
+
   Slabs slabs_of(const int2 *table, unsigned long long *err = nullptr) const {
     return Slabs{d_start, p, table, err};
   }
@@ -536,8 +761,38 @@ struct ShardedRun {
   }
 
   template <bool SPLIT, bool FROM_REF>
-  void events(Slab &x, const float *h, const int32_t *list, int n, int32_t *ext) {
+  void events(Slab &x, const float *h, const int32_t *list, int n, int32_t *ext,
+              const Track *tr = nullptr) {
     if (n <= 0) return;
+    if (!FROM_REF && cache_on && tr) {
+      // the stamp check re-emits the still valid results, the rest is walked
+      // (k_events_cached, which caches what stays inside the slab)
+      const EvCache ec = SPLIT ? x.ecP : x.ecJ;
+      int *todo = SPLIT ? x.todoP : x.todo, *ntodo = x.ntodo + (SPLIT ? 1 : 0);
+      CK(cudaMemsetAsync(ntodo, 0, sizeof(int), s));
+      k_events_check<SPLIT, true><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+          list, n, ec, *tr, x.marks, x.G, todo, ntodo, x.cnt, nullptr, nullptr, x.remote);
+      k_events_cached<SPLIT, true><<<148 * 16, 256, 0, s>>>(
+          h, list, todo, ntodo, x.slots, x.lm, ext, x.marks, x.G, ec, *tr, x.cnt, nullptr,
+          nullptr, slabs_of(SPLIT ? x.tup : x.tdn, x.cnt + C_CHANGED), x.remote);
+      CK(cudaGetLastError());
+      g_launches += 2;
+      return;
+    }
+    // g walks: 16 lanes per saddle (k_events16; a slab holds 1/p of the
+    // saddles, too few to hide a thread's walks in sequence)
+    // (a slab with many saddles keeps k_events: its waves hide the walks and
+    // 16 lanes per saddle issue more; A/B knob EXACTZ_SLAB_EV1: always k_events)
+    // (debug 0x2000000: k_events)
+    static const bool ev1 = std::getenv("EXACTZ_SLAB_EV1") != nullptr;
+    if (!FROM_REF && !ev1 && !(flags & 0x2000000u) && n <= (1 << 19)) {
+      k_events16<SPLIT, true><<<(unsigned)((16 * (int64_t)n + 255) / 256), 256, 0, s>>>(
+          h, list, n, x.slots, x.lm, ext, x.marks, x.G,
+          slabs_of(SPLIT ? x.tup : x.tdn, x.cnt + C_CHANGED), x.remote, x.cnt);
+      CK(cudaGetLastError());
+      g_launches++;
+      return;
+    }
     const int64_t threads = n;  // one lane per saddle
     k_events<SPLIT, FROM_REF, true><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
         h, list, n, x.slots, FROM_REF ? nullptr : x.lm, x.ref, ext, x.marks, x.G,
@@ -563,39 +818,71 @@ struct ShardedRun {
     const bool c3 = !(flags & EXACTZ_NO_C3);
     zero_counters();
     const bool c2 = !(flags & EXACTZ_NO_C2) && nS > 1;
+    ++rnd;
+    if (cache_on && rnd >= 65000) cache_on = false;  // 16-bit stamps (as exactz_correct)
+    const bool tracked = act_on || cache_on;  // the stencils / edit keep tracking state
     auto track = [&](Slab &x) {
       Track t{};
+      t.round = rnd;
+      t.tab_round = tab_round;
       if (act_on) {
         t.act_next = x.act[cur ^ 1];
         t.edited = x.edited;
       }
-      if (c2) {  // the stencils keep the owned entries of gS and list the changes
+      if (cache_on) {
+        t.bval = x.bval;
+        t.bslot = x.bslot;
+        t.sbval = x.sbval;
+        t.sbslot = x.sbslot;
+        t.nbx = x.nbx;
+        t.nby = x.nby;
+        t.nbz = x.nbz;
+        t.nsx = x.nsx;
+        t.nsy = x.nsy;
+      }
+      if (c2) {  // the stencils keep the owned entries of gS (k_gs_diff lists the changes)
         t.posS = x.posS;
         t.gS = x.gS;
-        t.gsupd = x.upd;
-        t.ngsupd = x.nrem + p + x.rank;
       }
       return t;
     };
     if (c2) each([&](Slab &x) { CK(cudaMemsetAsync(x.nrem + p, 0, p * 8, s)); });
+    if (c3 && !reform) each([&](Slab &x) { CK(cudaMemsetAsync(x.nrem + 2 * p, 0, p * 8, s)); });
     if (act_on && ready) {  // list-based pass: fired | stars of the last pass's edits
       halo_edited();
       each([&](Slab &x) {
         CK(cudaMemsetAsync(x.nlist, 0, sizeof(int), s));
         k_act_list<<<148 * 16, 256, 0, s>>>(x.act[cur], x.edited, x.G, x.list, x.nlist);
-        k_stencil_list<<<148 * 16, 256, 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm, x.list,
-                                                 x.nlist, x.G, track(x), x.cnt);
+        if (x.keyed)
+          k_stencil_list_key<<<148 * 16, 256, 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm, x.list,
+                                                       x.nlist, x.G, track(x), x.cnt);
+        else
+          k_stencil_list<<<148 * 16, 256, 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm, x.list,
+                                                   x.nlist, x.G, track(x), x.cnt);
       });
     } else {
       each([&](Slab &x) {
         const Track t = track(x);
-        if (x.fast && act_on)
+        const dim3 g2(x.sgrid.x, (unsigned)((ny + K2TY - 1) / K2TY), x.sgrid.z);
+        if (x.keyed && tracked && x.tma)
+          k_stencil_key2<true, true><<<g2, TX * K2W, 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
+                                                             x.G, x.zc, t, x.cnt, x.tmap);
+        else if (x.keyed && x.tma)
+          k_stencil_key2<false, true><<<g2, TX * K2W, 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
+                                                              x.G, x.zc, t, x.cnt, x.tmap);
+        else if (x.keyed && tracked)
+          k_stencil_key2<true, false><<<g2, TX * K2W, 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
+                                                              x.G, x.zc, t, x.cnt, x.tmap);
+        else if (x.keyed)
+          k_stencil_key2<false, false><<<g2, TX * K2W, 0, s>>>(x.g, x.ref, x.marks, x.slots,
+                                                               x.lm, x.G, x.zc, t, x.cnt, x.tmap);
+        else if (x.fast && tracked)
           k_stencil_fast<true><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
                                                                  x.G, x.zc, t, x.cnt);
         else if (x.fast)
           k_stencil_fast<false><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots,
                                                                  x.lm, x.G, x.zc, t, x.cnt);
-        else if (act_on)
+        else if (tracked)
           k_stencil<true><<<x.sgrid, dim3(TX, TY), 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm,
                                                            x.G, x.zc, t, x.cnt);
         else
@@ -616,34 +903,44 @@ struct ShardedRun {
                                                             C_N1 + 4);
       });
       CK(cudaGetLastError());
-    } else if (c3 && !reform) {
-      boundary_tables(false);
-      each([&](Slab &x) {
-        events<false, false>(x, x.g, x.J, x.nJ, x.m1);
-        events<true, false>(x, x.g, x.P, x.nP, x.M1);
-      });
     }
-    // one count exchange for the two sparse all-gathers of the round:
-    // nrem[0, p) = each rank's remote C3 targets, nrem[p, 2p) = each rank's
-    // changed gS entries (counted by the stencils); then C2 (R4) on the
-    // updated replicas and the owners' remote marks
     const bool c3w = c3 && !reform;
+    if (c2)
+      each([&](Slab &x) {
+        if (x.nown)
+          k_gs_diff<<<(x.nown + 255) / 256, 256, 0, s>>>(x.own, x.nown, x.gS, x.gSprev, x.upd,
+                                                         x.nrem + p + x.rank);
+      });
+    // the g boundary tables (C3 walks that leave a slab): this rank's entries
+    // recomputed; after the first pass only the changed ones travel
+    const size_t A2 = (size_t)nx * ny;
+    if (c3w)
+      each([&](Slab &x) {
+        CK(cudaMemsetAsync(x.nrem + 2 * p + x.rank, 0, 8, s));
+        const unsigned nb = (unsigned)((4 * A2 + 255) / 256);
+        if (cache_on)
+          k_boundary_delta<true><<<nb, 256, 0, s>>>(x.g, x.slots, x.G, x.rank, p, x.tdn, x.tupd,
+                                                    x.nrem + 2 * p + x.rank, track(x), x.brnd,
+                                                    x.bmask);
+        else
+          k_boundary_delta<false><<<nb, 256, 0, s>>>(x.g, x.slots, x.G, x.rank, p, x.tdn, x.tupd,
+                                                     x.nrem + 2 * p + x.rank);
+      });
+    CK(cudaGetLastError());
+    // exchange A (before C2 and the walks): nrem[p, 2p) = each rank's changed
+    // gS entries (counted by the stencils), nrem[2p, 3p) = its changed table
+    // entries; one count exchange sizes both sparse all-gathers
     if (c2 || c3w) {
       std::vector<unsigned long long *> nb;
-      each([&](Slab &x) {
-        CK(cudaMemsetAsync(x.nrem, 0, p * 8, s));
-        if (c3w)
-          CK(cudaMemcpyAsync(x.nrem + x.rank, x.cnt + C_NREMOTE, 8, cudaMemcpyDeviceToDevice, s));
-        nb.push_back(x.nrem);
-      });
-      T.allreduce_sum_u64(nb, 2 * p);
-      std::vector<unsigned long long> counts(2 * p);
-      CK(cudaMemcpyAsync(counts.data(), sl[0].nrem, 2 * p * 8, cudaMemcpyDeviceToHost, s));
+      each([&](Slab &x) { nb.push_back(x.nrem); });
+      T.allreduce_sum_u64(nb, 3 * p);
+      std::vector<unsigned long long> counts(3 * p);
+      CK(cudaMemcpyAsync(counts.data(), sl[0].nrem, 3 * p * 8, cudaMemcpyDeviceToHost, s));
       sync();
-      unsigned long long mr = 0, mu = 0;
+      unsigned long long mu = 0, mt = 0;
       for (int r = 0; r < p; ++r) {
-        mr = std::max(mr, counts[r]);
         mu = std::max(mu, counts[p + r]);
+        mt = std::max(mt, counts[2 * p + r]);
       }
       if (c2 && mu) {
         std::vector<const void *> snd;
@@ -660,19 +957,82 @@ struct ShardedRun {
           k_apply_gs<<<(n + 255) / 256, 256, 0, s>>>(x.allupd, n, x.gS);
         });
       }
-      if (c2)
-        each([&](Slab &x) {
-          k_saddle_order_slab<<<(nS + 255) / 256, 256, 0, s>>>(x.gS, x.S, nS, x.marks, x.G, x.cnt);
+      // (debug 0x800000: sparse after the first pass, whatever the count;
+      // 0x1000000: whole chunks every pass)
+      const bool full = !tables_ready || (flags & 0x1000000u) ||
+                        (2 * mt > A2 && !(flags & 0x800000u));
+      if (c3w && full) {
+        // the first pass (or many changes): every rank's whole chunk, in place
+        for (int up = 0; up < 2; ++up) {
+          std::vector<const void *> snd;
+          std::vector<void *> rcv;
+          each([&](Slab &x) {
+            int2 *t = up ? x.tup : x.tdn;
+            snd.push_back(t + 2 * A2 * x.rank);
+            rcv.push_back(t);
+          });
+          T.allgather(snd, rcv, 2 * A2 * sizeof(int2));
+        }
+        tables_ready = true;
+        tab_round = rnd;
+      } else if (c3w && mt) {
+        tab_round = rnd;  // (cached walks that used the tables are stale)
+        if (mt * p > x_alltupd_cap()) grow_alltupd(mt * p);
+        std::vector<const void *> snd;
+        std::vector<void *> rcv;
+        each([&](Slab &x) {  // pad to mt with position -1
+          const unsigned long long c = counts[2 * p + x.rank];
+          if (mt > c) CK(cudaMemsetAsync(x.tupd + c, 0xff, (mt - c) * 16, s));
+          snd.push_back(x.tupd);
+          rcv.push_back(x.alltupd);
         });
-      if (c3w && mr) {
+        T.allgather(snd, rcv, mt * 16);
+        each([&](Slab &x) {
+          const int n = (int)(mt * p);
+          k_apply_tab<<<(n + 255) / 256, 256, 0, s>>>(x.alltupd, n, x.tdn);
+        });
+      }
+      CK(cudaGetLastError());
+    }
+    // C2 (R4) on the updated replicas, the owned pairs only
+    if (c2)
+      each([&](Slab &x) {
+        if (x.nown)
+          k_saddle_order_slab<<<(x.nown + 255) / 256, 256, 0, s>>>(x.gS, x.S, nS, x.marks, x.G,
+                                                                   x.cnt, C_N1 + 3, x.own, x.nown);
+      });
+    if (c3w)
+      each([&](Slab &x) {
+        const Track t = track(x);
+        events<false, false>(x, x.g, x.J, x.nJ, x.m1, &t);
+        events<true, false>(x, x.g, x.P, x.nP, x.M1, &t);
+      });
+    CK(cudaGetLastError());
+    // exchange B: the walks' targets owned by another rank (all-gathered)
+    if (c3w) {
+      std::vector<unsigned long long *> nb;
+      each([&](Slab &x) {
+        CK(cudaMemsetAsync(x.nrem, 0, p * 8, s));
+        CK(cudaMemcpyAsync(x.nrem + x.rank, x.cnt + C_NREMOTE, 8, cudaMemcpyDeviceToDevice, s));
+        nb.push_back(x.nrem);
+      });
+      T.allreduce_sum_u64(nb, p);
+      std::vector<unsigned long long> counts(p);
+      CK(cudaMemcpyAsync(counts.data(), sl[0].nrem, p * 8, cudaMemcpyDeviceToHost, s));
+      sync();
+      unsigned long long mr = 0;
+      for (int r = 0; r < p; ++r) mr = std::max(mr, counts[r]);
+      if (mr) {
         std::vector<const void *> snd;
         std::vector<void *> rcv;
         each([&](Slab &x) {
-          int32_t *pad = A.get<int32_t>(mr);
-          CK(cudaMemsetAsync(pad, 0xff, mr * 4, s));  // -1: no vertex
-          CK(cudaMemcpyAsync(pad, x.remote, counts[x.rank] * 4, cudaMemcpyDeviceToDevice, s));
-          x.allremote = A.get<int32_t>(mr * p);
-          snd.push_back(pad);
+          if (mr * p > x.allremote_cap) {
+            x.allremote_cap = 2 * mr * p;
+            x.allremote = A.get<int32_t>(x.allremote_cap);
+          }
+          if (mr > counts[x.rank])
+            CK(cudaMemsetAsync(x.remote + counts[x.rank], 0xff, (mr - counts[x.rank]) * 4, s));
+          snd.push_back(x.remote);
           rcv.push_back(x.allremote);
         });
         T.allgather(snd, rcv, mr * 4);
@@ -707,8 +1067,8 @@ struct ShardedRun {
       CK(cudaGetLastError());
     }
     each([&](Slab &x) {
-      if (act_on) {
-        CK(cudaMemsetAsync(x.edited, 0, (size_t)x.G.nz * x.words_per_plane() * 4, s));
+      if (tracked) {
+        if (act_on) CK(cudaMemsetAsync(x.edited, 0, (size_t)x.G.nz * x.words_per_plane() * 4, s));
         k_count_edit<true><<<148 * 8, 256, 0, s>>>(x.g, x.c, x.marks, x.f, x.G, xi, delta, N,
                                                     do_edit ? 1 : 0, track(x), x.cnt);
       } else {
@@ -729,6 +1089,11 @@ struct ShardedRun {
     }
     for (int k = 0; k < 8; ++k) out[k] = sl[0].hcnt[k];
     halo_planes(false);  // the edited boundary planes refresh the neighbours' ghosts
+    if (cache_on)        // ... and their changes stamp the ghost bricks (C3 cache)
+      each([&](Slab &x) {
+        k_ghost_stamp<<<(unsigned)((2 * x.plane() + 255) / 256), 256, 0, s>>>(x.g, x.ghost_prev,
+                                                                              x.G, track(x));
+      });
   }
 };
 
@@ -751,15 +1116,7 @@ static exactz_status sharded_impl(Transport &T, std::vector<const float *> f_in,
   uint32_t max_iters = opts ? opts->max_iters : 0u;
   exactz_stats *stats = opts ? opts->stats : nullptr;
   Ctx::keep_pool();
-  {
-    static thread_local uint8_t lut[1 << kSlots];
-    static thread_local bool ready = false;
-    if (!ready) {
-      for (uint32_t m = 0; m < (1u << kSlots); ++m) lut[m] = (uint8_t)link_components_t(m, kLink.adj);
-      ready = true;
-    }
-    CK(cudaMemcpyToSymbolAsync(d_comp, lut, sizeof(lut), 0, cudaMemcpyHostToDevice, s));
-  }
+  upload_luts(s);
   Arena A(s);
   std::vector<Slab> slabs(T.nlocal());
   struct HostFree {
@@ -780,6 +1137,20 @@ static exactz_status sharded_impl(Transport &T, std::vector<const float *> f_in,
     // from the globally reduced V_t (the same decision on every rank)
     if (!(flags & EXACTZ_NO_TRACK) && !R.act_on && rows >= 1 && prev_vt * 8 <= (unsigned long long)V)
       R.start_act();
+    // the C3 cache once the marks are sparse at brick scale (exactz_correct's
+    // rule over the global brick grid; debug 0x200: off)
+    {
+      static const unsigned long long cache_div = [] {
+        const char *e = std::getenv("EXACTZ_SLAB_CACHE_DIV");  // A/B knob (dev)
+        if (!e) e = std::getenv("EXACTZ_CACHE_DIV");
+        return e ? std::strtoull(e, nullptr, 10) : 4ull;
+      }();
+      const unsigned long long nbg = (unsigned long long)((dims[0] + BX - 1) / BX) *
+                                     ((dims[1] + BY - 1) / BY) * ((dims[2] + BZ - 1) / BZ);
+      if (!(flags & (EXACTZ_NO_TRACK | EXACTZ_REFORMULATED | 0x200u)) && !R.cache_on && rows >= 1 &&
+          rows < 65000 && prev_vt * cache_div <= nbg)
+        R.start_cache();
+    }
     unsigned long long o[8];
     R.round(may_edit, o);
     prev_vt = o[C_VT];
