@@ -210,8 +210,8 @@ exactz_status exactz_comm_destroy(exactz_comm *comm);
 /* f_local / g_local / out_local: the z_count planes [z_begin, z_begin+z_count)
  * of the global field (global_dims = {nx, ny, nz}); rank r must own exactly
  * the planes of the split "the first nz % nranks ranks get one extra plane"
- * (else EXACTZ_EINVAL).  label_min/max are not supported (EXACTZ_EUNSUPPORTED);
- * edit_counts covers the local planes.  out_local is bit-equal to
+ * (else EXACTZ_EINVAL).  edit_counts, label_min and label_max cover the local
+ * planes (labels are global vertex ids, equal to exactz_correct's).  out_local is bit-equal to
  * the same planes of the single-GPU out; *iters identical on every rank. */
 exactz_status exactz_correct_sharded(exactz_comm *comm, const float *f_local,
                                      const float *g_local, const int64_t global_dims[3],
@@ -222,8 +222,8 @@ exactz_status exactz_correct_sharded(exactz_comm *comm, const float *f_local,
 /* Single-process slab decomposition: runs the sharded algorithm with
  * `nslabs` virtual ranks on the current device (loopback transport instead of
  * NCCL); f, g_in, out are whole-field device buffers.  Validates the sharded
- * path on one GPU: out is bit-equal to exactz_correct's.  label_min/max are
- * not supported (EXACTZ_EUNSUPPORTED). */
+ * path on one GPU: out (and edit_counts, label_min, label_max: whole-field
+ * buffers) is bit-equal to exactz_correct's. */
 exactz_status exactz_correct_slabs(const float *f, const float *g_in, const int64_t dims[3],
                                    float eps_abs, int nslabs, float *out, uint32_t *iters,
                                    const exactz_opts *opts, void *stream);

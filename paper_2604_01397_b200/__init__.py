@@ -310,14 +310,15 @@ def exactz_slab_range(nz: int, nranks: int, rank: int):
 
 
 def exactz_correct_slabs(f, g_in, eps: float, nslabs: int, out=None, *, N: int = 5,
-                         max_iters: int = 0, flags: int = 0, edit_counts=None,
-                         stats_cap: int = 0, stream=None) -> CorrectResult:
+                         max_iters: int = 0, flags: int = 0, edit_counts=None, label_min=None,
+                         label_max=None, stats_cap: int = 0, stream=None) -> CorrectResult:
     """The sharded algorithm with `nslabs` virtual ranks on the current GPU
-    (loopback transport): bit-equal to exactz_correct."""
+    (loopback transport): bit-equal to exactz_correct (out, edit_counts and
+    the whole-field int32 label outputs)."""
     import torch
     if out is None:
         out = torch.empty_like(g_in)
-    o, st, rows = _opts(N, max_iters, flags, edit_counts, None, None, stats_cap)
+    o, st, rows = _opts(N, max_iters, flags, edit_counts, label_min, label_max, stats_cap)
     iters = C.c_uint32(0)
     s = _lib.exactz_correct_slabs(_ptr(f), _ptr(g_in), _dims(f), float(eps), nslabs, _ptr(out),
                                   C.byref(iters), C.byref(o), _stream(stream))
@@ -355,14 +356,16 @@ class Comm:
 
 def exactz_correct_sharded(comm: Comm, f_local, g_local, global_dims, eps: float, out=None, *,
                            N: int = 5, max_iters: int = 0, flags: int = 0, edit_counts=None,
-                           stats_cap: int = 0, stream=None) -> CorrectResult:
+                           label_min=None, label_max=None, stats_cap: int = 0,
+                           stream=None) -> CorrectResult:
     """One rank of the z-slab decomposition: f_local/g_local are this rank's
-    planes (shape (z_count, ny, nx)); collective over comm."""
+    planes (shape (z_count, ny, nx)); collective over comm.  edit_counts and
+    the int32 label outputs cover the local planes (labels: global ids)."""
     import torch
     if out is None:
         out = torch.empty_like(g_local)
     z0, zc = exactz_slab_range(int(global_dims[2]), comm.nranks, comm.rank)
-    o, st, rows = _opts(N, max_iters, flags, edit_counts, None, None, stats_cap)
+    o, st, rows = _opts(N, max_iters, flags, edit_counts, label_min, label_max, stats_cap)
     iters = C.c_uint32(0)
     dims = (C.c_int64 * 3)(*[int(x) for x in global_dims])
     s = _lib.exactz_correct_sharded(comm.h, _ptr(f_local), _ptr(g_local), dims, z0, zc,

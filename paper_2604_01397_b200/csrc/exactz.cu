@@ -1890,7 +1890,8 @@ exactz_status exactz_correct_sharded(exactz_comm *comm, const float *f_local, co
     }
     NcclTransport T(comm, (cudaStream_t)stream);
     return sharded_impl(T, {f_local}, {g_local}, {out_local},
-                        {opts ? opts->edit_counts : nullptr}, global_dims, eps_abs, iters, opts,
+                        {opts ? opts->edit_counts : nullptr}, {opts ? opts->label_min : nullptr},
+                        {opts ? opts->label_max : nullptr}, global_dims, eps_abs, iters, opts,
                         (cudaStream_t)stream);
   });
 }
@@ -1909,6 +1910,7 @@ exactz_status exactz_correct_slabs(const float *f, const float *g_in, const int6
     std::vector<const float *> fi, gi;
     std::vector<float *> o;
     std::vector<uint8_t *> co;
+    std::vector<int32_t *> ln, lx;
     const size_t P = (size_t)dims[0] * dims[1];
     for (int r = 0; r < nslabs; ++r) {
       int64_t z0 = 0, cnt = 0;
@@ -1917,8 +1919,10 @@ exactz_status exactz_correct_slabs(const float *f, const float *g_in, const int6
       gi.push_back(g_in + z0 * P);
       o.push_back(out + z0 * P);
       co.push_back(opts && opts->edit_counts ? opts->edit_counts + z0 * P : nullptr);
+      ln.push_back(opts && opts->label_min ? opts->label_min + z0 * P : nullptr);
+      lx.push_back(opts && opts->label_max ? opts->label_max + z0 * P : nullptr);
     }
-    return sharded_impl(T, fi, gi, o, co, dims, eps_abs, iters, opts, s);
+    return sharded_impl(T, fi, gi, o, co, ln, lx, dims, eps_abs, iters, opts, s);
   });
 }
 

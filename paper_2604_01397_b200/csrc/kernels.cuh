@@ -2423,6 +2423,39 @@ __global__ void k_boundary_delta(const float *__restrict__ h, const uint8_t *__r
   const long long q = cta_slot(chg, nupd);  // (a dense pass changes most entries)
   if (q >= 0) upd[q] = make_int4(pos, val.x, val.y, 0);
 }
+// Labels of a slab's owned vertices (the optional label outputs of the
+// sharded call): the steepest pointers of the final field inside the slab
+// (a pointer into a ghost plane becomes the exit -(global id + 1)), local
+// pointer jumping, then exits completed from the boundary tables.
+__global__ void k_slab_ptrs(const uint8_t *__restrict__ slots, int32_t *p, GridP G, int up) {
+  const int A = G.nx * G.ny, lo = G.zb * A, hi = G.ze * A;
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hi) return;
+  const int t = slot_target(i, (slots[i] >> (up ? 4 : 0)) & 15, G);
+  p[i] = (t >= lo && t < hi) ? t : -(t + G.zoff * A) - 1;
+}
+__global__ void k_jump_slab(int32_t *lab, GridP G, unsigned long long *changed) {
+  const int A = G.nx * G.ny, lo = G.zb * A, hi = G.ze * A;
+  unsigned c = 0;
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x) {
+    const int w = lab[i];
+    if (w < 0) continue;  // an exit: resolved by the tables
+    const int w2 = lab[w];
+    if (w2 != w) {
+      lab[i] = w2;
+      c = 1;
+    }
+  }
+  if (__any_sync(0xffffffffu, c) && (threadIdx.x & 31) == 0) atomicOr(changed, 1ull);
+}
+__global__ void k_slab_resolve(const int32_t *__restrict__ lab, GridP G, Slabs S, int32_t *out) {
+  const int A = G.nx * G.ny, lo = G.zb * A, hi = G.ze * A;
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hi) return;
+  const int w = lab[i];
+  out[i - lo] = w >= 0 ? w + G.zoff * A : table_lookup(S, -w - 1, A).x;
+}
+
 // A slab's ghost planes after the halo refresh: a vertex whose value changed
 // (the neighbour's edit of its boundary plane) stamps its brick as an edit of
 // this pass does (round + 1), so the C3 cache sees a saddle star or a walk

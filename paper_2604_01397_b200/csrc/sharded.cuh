@@ -801,6 +801,47 @@ struct ShardedRun {
     CK(cudaGetLastError());
   }
 
+  // Labels of the final field (optional outputs): the boundary tables of its
+  // slots (recomputed whole, whatever the passes kept), then per slab local
+  // pointer jumping and the exits through the tables.  lo_out / hi_out: the
+  // owned planes of label_min / label_max per local rank (nullptr: not wanted)
+  void labels(const std::vector<int32_t *> &dn_out, const std::vector<int32_t *> &up_out) {
+    boundary_tables(false);
+    for (int up = 0; up < 2; ++up) {
+      int l = 0;
+      each([&](Slab &x) {
+        int32_t *dst = (up ? up_out : dn_out)[l++];
+        if (!dst) return;
+        const int n = x.nzl * (int)x.plane();
+        int32_t *lab = A.get<int32_t>((size_t)x.G.V);
+        k_slab_ptrs<<<(n + 255) / 256, 256, 0, s>>>(x.slots, lab, x.G, up);
+        for (int round = 0;; ++round) {
+          if (round > 64) {
+            set_err("labels", "pointer jumping did not converge");
+            throw Error{EXACTZ_ECUDA};
+          }
+          CK(cudaMemsetAsync(x.cnt + C_CHANGED, 0, 8, s));
+          k_jump_slab<<<blocks_for(n, 256), 256, 0, s>>>(lab, x.G, x.cnt + C_CHANGED);
+          unsigned long long ch = 0;
+          CK(cudaMemcpyAsync(&ch, x.cnt + C_CHANGED, 8, cudaMemcpyDeviceToHost, s));
+          sync();
+          if (!ch) break;
+        }
+        CK(cudaMemsetAsync(x.cnt + C_CHANGED, 0, 8, s));
+        k_slab_resolve<<<(n + 255) / 256, 256, 0, s>>>(lab, x.G, slabs_of(up ? x.tup : x.tdn,
+                                                                          x.cnt + C_CHANGED), dst);
+        unsigned long long bad = 0;
+        CK(cudaMemcpyAsync(&bad, x.cnt + C_CHANGED, 8, cudaMemcpyDeviceToHost, s));
+        sync();
+        if (bad) {
+          set_err("labels", "an exit chain is longer than the table (a cycle)");
+          throw Error{EXACTZ_ECUDA};
+        }
+      });
+    }
+    CK(cudaGetLastError());
+  }
+
   // Sums counters [0, n) over the ranks.  Per pass only C_VT .. C_BAD_BOUND
   // are global; C_NREMOTE / C_WALK stay per rank.
   void allreduce_counters(int n = C_BAD_BOUND + 1) {
@@ -1099,7 +1140,9 @@ struct ShardedRun {
 
 static exactz_status sharded_impl(Transport &T, std::vector<const float *> f_in,
                                   std::vector<const float *> g_in, std::vector<float *> out,
-                                  std::vector<uint8_t *> counts_out, const int64_t dims[3],
+                                  std::vector<uint8_t *> counts_out,
+                                  std::vector<int32_t *> lmin_out, std::vector<int32_t *> lmax_out,
+                                  const int64_t dims[3],
                                   float eps, uint32_t *iters, const exactz_opts *opts,
                                   cudaStream_t s) {
   int64_t V = 0;
@@ -1107,10 +1150,6 @@ static exactz_status sharded_impl(Transport &T, std::vector<const float *> f_in,
   if (!std::isfinite(eps) || !(eps >= 0.0f)) return EXACTZ_EINVAL;
   int N = (opts && opts->N) ? (int)opts->N : 5;
   if (N < 1 || N > 254) return EXACTZ_EINVAL;
-  if (opts && (opts->label_min || opts->label_max)) {
-    set_err("exactz_correct_sharded", "label outputs are not supported by the sharded path");
-    return EXACTZ_EUNSUPPORTED;
-  }
   if (dims[2] < T.nranks()) return EXACTZ_EINVAL;  // every rank owns >= 1 plane
   uint32_t flags = opts ? opts->flags : 0u;
   uint32_t max_iters = opts ? opts->max_iters : 0u;
@@ -1172,6 +1211,8 @@ static exactz_status sharded_impl(Transport &T, std::vector<const float *> f_in,
     }
     ++it;
   }
+  // labels of the final field: its slots are the last pass's (no edit followed)
+  if (opts && (opts->label_min || opts->label_max)) R.labels(lmin_out, lmax_out);
   for (size_t l = 0; l < slabs.size(); ++l) {
     Slab &x = slabs[l];
     const size_t P = x.plane();

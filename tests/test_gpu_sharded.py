@@ -84,6 +84,29 @@ def test_slabs_engine_variants(exactz, flags):
     assert_same(*both(exactz, f, g, xi, 6, flags=flags))
 
 
+@pytest.mark.parametrize("cfg,shape,p,kw", [("C1", None, 3, {}), ("C3", (12, 16, 50), 12, {}),
+                                            ("C2", (20, 24, 70), 4, {"flags": 2}),
+                                            ("C5", (9, 12, 33), 8, {"flags": 0x10})])
+def test_slabs_labels(exactz, oracle, cfg, shape, p, kw):
+    """label_min / label_max of the sharded call (local pointer jumping, exits
+    through the boundary tables; recomputed at the end when the passes kept no
+    tables: NO_C3, reformulated) equal the single-GPU call's and the oracle's."""
+    f, g, xi = S.make(cfg, shape=shape) if shape else S.make(cfg)
+    V = f.numel()
+    fd, gd = f.cuda(), g.cuda()
+    la, lb = (torch.empty(V, dtype=torch.int32, device="cuda") for _ in range(2))
+    ua, ub = (torch.empty(V, dtype=torch.int32, device="cuda") for _ in range(2))
+    a = exactz.exactz_correct(fd, gd, xi, label_min=la, label_max=ua, **kw)
+    b = exactz.exactz_correct_slabs(fd, gd, xi, p, label_min=lb, label_max=ub, **kw)
+    torch.cuda.synchronize()
+    assert b.iters == a.iters and torch.equal(a.out.view(torch.int32), b.out.view(torch.int32))
+    assert torch.equal(la, lb) and torch.equal(ua, ub)
+    if not kw:
+        r = oracle.correct(f.numpy(), g.numpy(), xi, 5)
+        assert np.array_equal(lb.cpu().numpy(), r.label_min)
+        assert np.array_equal(ub.cpu().numpy(), r.label_max)
+
+
 @pytest.mark.parametrize("p", [2, 5])
 def test_slabs_reformulated(exactz, p):
     f, g, xi = S.make("C3", shape=(15, 20, 40))
@@ -119,16 +142,19 @@ def test_nccl_transport_one_rank(exactz, cfg, shape):
     fd, gd = f.cuda(), g.cuda()
     c1 = torch.empty(f.numel(), dtype=torch.uint8, device="cuda")
     c2 = torch.empty_like(c1)
-    a = exactz.exactz_correct(fd, gd, xi, edit_counts=c1, stats_cap=100000)
+    la, lb, ua, ub = (torch.empty(f.numel(), dtype=torch.int32, device="cuda") for _ in range(4))
+    a = exactz.exactz_correct(fd, gd, xi, edit_counts=c1, label_min=la, label_max=ua,
+                              stats_cap=100000)
     comm = exactz.Comm(exactz.exactz_nccl_unique_id(), 1, 0, torch.cuda.current_device())
     try:
         dims = (f.shape[2], f.shape[1], f.shape[0])
-        b = exactz.exactz_correct_sharded(comm, fd, gd, dims, xi, edit_counts=c2,
-                                          stats_cap=100000)
+        b = exactz.exactz_correct_sharded(comm, fd, gd, dims, xi, edit_counts=c2, label_min=lb,
+                                          label_max=ub, stats_cap=100000)
         torch.cuda.synchronize()
     finally:
         comm.close()
     assert_same(a, b, c1, c2)
+    assert torch.equal(la, lb) and torch.equal(ua, ub)
 
 
 def test_slabs_long_exit_chains(exactz):
