@@ -1715,11 +1715,21 @@ __global__ void __launch_bounds__(256) k_events16(const float *__restrict__ h,
                                                   const int32_t *__restrict__ ref_ext,
                                                   uint32_t *marks, GridP G, Slabs S,
                                                   int32_t *remote, unsigned long long *cnt,
-                                                  const int32_t *__restrict__ lpos = nullptr) {
-  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+                                                  const int32_t *__restrict__ lpos = nullptr,
+                                                  const int *__restrict__ idx = nullptr,
+                                                  const int *__restrict__ nidx = nullptr) {
+  // idx: the saddles idx[0 .. *nidx) (k_fclean's list; *nidx < 0: the test
+  // was skipped, every saddle); else all n
+  int nact = idx ? *nidx : n;
+  if (nact < 0) {
+    nact = n;
+    idx = nullptr;
+  }
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
   const int l16 = threadIdx.x & 15;
   const unsigned gmask = 0xffffu << (threadIdx.x & 16);  // this 16-lane group
-  const bool active = k < n;
+  const bool active = g < nact;
+  const int k = active && idx ? __ldg(&idx[g]) : g;
   const int A = G.nx * G.ny, off = G.zoff * A, lo = G.zb * A, hi = G.ze * A;
   int s = 0;
   uint32_t todo = 0;
@@ -2046,7 +2056,11 @@ struct FPaths {
 // one contiguous run for its 32 lists (k_fclean scans it coalesced).
 constexpr int kFTileCap = 512;
 static_assert(kFTileCap <= 65535, "FPaths::len is 16-bit");
-template <bool SPLIT>
+// SLAB (a z-slab of the sharded call): ids local to the slab (lab[] holds
+// local vertex ids; k_fclean adds the offset), a walk that leaves the owned
+// planes makes its saddle "always walked" (its tiles beyond are another
+// rank's), and ext (m1 / M1, from the boundary tables) is not written.
+template <bool SPLIT, bool SLAB = false>
 __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, int n,
                                                 const uint32_t *__restrict__ ref, GridP G,
                                                 int ntx, int nty, unsigned long long *bump,
@@ -2079,8 +2093,10 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
 #pragma unroll
   for (int j = 0; j < kFLab; ++j) lb[j] = -1;
   unsigned long long mask = 0;
+  bool exited = false;
   if (act) {
-    const int s = __ldg(&sl[k]);
+    const int A = G.nx * G.ny, lo = G.zb * A, hi = G.ze * A;
+    const int s = __ldg(&sl[k]) - (SLAB ? G.zoff * A : 0);
     const int yz = div_nx(s, G), sz = div_ny(yz, G);
     const int sx = s - yz * G.nx, sy = yz - sz * G.ny;
     const uint32_t valid = valid_mask(sx, sy, sz, G), flow = ref_flow(__ldg(&ref[s]));
@@ -2102,6 +2118,10 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
       int p = sdel[q], w = s + soff[q];
       int x = sx + (p & 3) - 1, y = sy + ((p >> 2) & 3) - 1, z = sz + (p >> 4) - 1;
       for (;;) {
+        if (SLAB && (w < lo || w >= hi)) {
+          exited = true;
+          break;
+        }
         const int t = ftile(x, y, z, ntx, nty);
         if (t != last && t != last2) {
           if (e < kFTileCap) buf[e] = t;
@@ -2119,8 +2139,9 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
         y += ((p >> 2) & 3) - 1;
         z += (p >> 4) - 1;
       }
+      if (SLAB && exited) break;
       {  // a terminus: m1 / M1 and X_f
-        const float val = f[w];
+        const float val = SLAB ? 0.0f : f[w];
         bool take;
         if (best < 0) take = true;
         else if (!SPLIT) take = (bv < val) || (bv == val && best < w);  // SoS max
@@ -2141,7 +2162,7 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
   // one reservation per warp, lists in lane order
   const int lane = threadIdx.x & 31;
   // (a reserved run holds no holes: k_fclean scans the warp's run whole)
-  const bool want = act && e <= kFTileCap && nl <= kFLab;
+  const bool want = act && e <= kFTileCap && nl <= kFLab && !exited;
   const int c = want ? e : 0;
   int inc = c;
 #pragma unroll
@@ -2171,7 +2192,7 @@ __global__ void __launch_bounds__(256) k_fpaths(const int32_t *__restrict__ sl, 
   nlab[k] = (uint8_t)(ok ? nl : 255);  // 255: always walked
 #pragma unroll
   for (int j = 0; j < kFLab; ++j) lab[(size_t)k * kFLab + j] = lb[j];
-  ext[k] = best;
+  if (!SLAB) ext[k] = best;
 }
 
 // CTA-aggregated append of k to todo for the threads with `need` (one atomic
@@ -2238,7 +2259,9 @@ __device__ __forceinline__ long long cta_slot(bool need, unsigned long long *n) 
 // result is cached with the bricks of its star and f-walks (its g-walks), so
 // later passes re-emit it while those bricks are unchanged.  Grid-stride
 // (block-uniform trip count): a launch over a short idx list stays small.
-template <bool SPLIT>
+// SLAB: saddle ids global, F.lab local (see k_fpaths), a target in another
+// slab goes to `remote`
+template <bool SPLIT, bool SLAB = false>
 __global__ void __launch_bounds__(256) k_fclean(const float *__restrict__ g,
                                                 const int32_t *__restrict__ sl, int n,
                                                 const uint32_t *__restrict__ lm,
@@ -2249,7 +2272,9 @@ __global__ void __launch_bounds__(256) k_fclean(const float *__restrict__ g,
                                                 const int *__restrict__ idx,
                                                 const int *__restrict__ nidx, EvCache EC,
                                                 int round, const unsigned long long *ndirt,
-                                                unsigned long long max_dirt) {
+                                                unsigned long long max_dirt,
+                                                int32_t *remote = nullptr) {
+  const int A = G.nx * G.ny, off = SLAB ? G.zoff * A : 0;
   // gate: with more than max_dirt dirty tiles few saddles are clean; the
   // test is skipped and the walk kernels take every saddle (*ntodo = -1)
   if (*ndirt > max_dirt) {
@@ -2268,7 +2293,7 @@ __global__ void __launch_bounds__(256) k_fclean(const float *__restrict__ g,
     bool need = false;
     int s = 0, nl = 0;
     if (act) {
-      s = __ldg(&sl[k]);
+      s = __ldg(&sl[k]) - off;
       nl = F.nlab[k];
       need = nl > kFLab || ((saddle_lm(lm, F.lpos, k, s) ^ F.flow[k]) & 0x3FFFu) != 0;
     }
@@ -2318,9 +2343,11 @@ __global__ void __launch_bounds__(256) k_fclean(const float *__restrict__ g,
       }
       const int want = __ldg(&ref_ext[k]);
       int target = -1;
-      if (best >= 0 && best != want) {
-        target = SPLIT ? want : best;
-        mark_vertex(marks, target, G);
+      if (best >= 0 && best + off != want) {
+        target = SPLIT ? want : best + off;  // global
+        const int t = target - off;
+        if (!SLAB || (t >= G.zb * A && t < G.ze * A)) mark_vertex(marks, t, G);
+        else remote[atomicAdd(&cnt[C_NREMOTE], 1ull)] = target;
         ++hit;
       }
       if (EC.rnd) {

@@ -300,6 +300,12 @@ struct Slab {
   uint16_t *bval = nullptr, *bslot = nullptr, *sbval = nullptr, *sbslot = nullptr;
   EvCache ecJ{}, ecP{};
   int *todo = nullptr, *todoP = nullptr, *ntodo = nullptr;
+  // the clean-path test of the C3 walks (exactz_correct's FPaths, slab-local)
+  FPaths fpJ{}, fpP{};
+  uint8_t *dirtD = nullptr, *dirtU = nullptr;
+  unsigned long long *ndirt = nullptr;
+  int ntx = 0, nty = 0, nt = 0;
+  int *ftodo = nullptr, *ftodoP = nullptr, *nftodo = nullptr;
   float *ghost_prev = nullptr;         // the ghost planes' values as last stamped
   uint16_t *brnd = nullptr;            // boundary-table entries: round and bricks of the
   unsigned long long *bmask = nullptr; // last walk (k_boundary_delta<true>)
@@ -320,6 +326,7 @@ struct ShardedRun {
   uint32_t flags;
   bool act_on = false, ready = false;  // vertex activity started / act[cur] valid
   bool cache_on = false;               // the C3 cache started
+  bool fp_on = false;                  // the clean-path test is set up (list passes use it)
   int rnd = 0;                         // pass number (16-bit stamps of the cache)
   int tab_round = 0;                   // last pass in which a g boundary-table entry changed
   bool tables_ready = false;           // the g boundary tables hold a previous pass's
@@ -364,6 +371,72 @@ struct ShardedRun {
     });
     act_on = true;
   }
+  // The clean-path test (exactz_correct's Tracking::start_fpaths): the f-walks
+  // of every saddle inside its slab, their tiles and f-labels; a saddle whose
+  // f-walks leave the slab is always walked.  gate: see exactz_correct.
+  void start_fpaths(double gate) {
+    each([&](Slab &x) {
+      x.ntx = (nx + (1 << FTX_SH) - 1) >> FTX_SH;
+      x.nty = (ny + (1 << FTY_SH) - 1) >> FTY_SH;
+      const int ntz = (x.G.nz + (1 << FTZ_SH) - 1) >> FTZ_SH;
+      x.nt = x.ntx * x.nty * ntz;
+      const size_t nt16 = ((size_t)x.nt + 15) / 16 * 16;
+      x.dirtD = A.get<uint8_t>(2 * nt16 + 16);
+      x.dirtU = x.dirtD + nt16;
+      x.ndirt = reinterpret_cast<unsigned long long *>(x.dirtD + 2 * nt16);
+      unsigned long long *bump = A.get<unsigned long long>(2);
+      CK(cudaMemsetAsync(bump, 0, 16, s));
+      auto alloc = [&](int n) {
+        FPaths F{};
+        const size_t m = n ? (size_t)n : 1;
+        F.off = A.get<int64_t>(m);
+        F.len = A.get<uint16_t>(m);
+        F.lab = A.get<int32_t>(m * kFLab);
+        F.nlab = A.get<uint8_t>(m);
+        F.bmask = A.get<unsigned long long>(m);
+        F.flow = A.get<uint16_t>(m);
+        F.cap = 24ull * m + 4096;
+        F.tiles = A.get<int32_t>(F.cap);
+        return F;
+      };
+      x.fpJ = alloc(x.nJ);
+      x.fpP = alloc(x.nP);
+      for (int sp = 0; sp < 2; ++sp) {
+        const FPaths &F = sp ? x.fpP : x.fpJ;
+        const int n = sp ? x.nP : x.nJ;
+        if (n <= 0) continue;
+        auto go = [&](auto kern) {
+          kern<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+              sp ? x.P : x.J, n, x.ref, x.G, x.ntx, x.nty, bump + sp, F.cap,
+              const_cast<int64_t *>(F.off), const_cast<uint16_t *>(F.len),
+              const_cast<int32_t *>(F.tiles), const_cast<int32_t *>(F.lab),
+              const_cast<uint8_t *>(F.nlab), const_cast<unsigned long long *>(F.bmask), nullptr,
+              x.f, nullptr, const_cast<uint16_t *>(F.flow), nullptr);
+        };
+        if (sp) go(k_fpaths<true, true>);
+        else go(k_fpaths<false, true>);
+      }
+      CK(cudaGetLastError());
+      unsigned long long h[2] = {0, 0};
+      CK(cudaMemcpyAsync(h, bump, sizeof(h), cudaMemcpyDeviceToHost, s));
+      sync();
+      for (int sp = 0; sp < 2; ++sp) {
+        FPaths &F = sp ? x.fpP : x.fpJ;
+        const int n = sp ? x.nP : x.nJ;
+        const double L = n ? (double)h[sp] / n : 0.0;
+        const double fr = gate > 0.0 && L > 0.0 ? 1.0 - std::pow(gate, 1.0 / L) : 1.0;
+        F.max_dirt = gate > 0.0 ? (unsigned long long)(fr * x.nt) : ~0ull;
+        F.dirt = sp ? x.dirtU : x.dirtD;
+        F.nt = x.nt;
+        F.ndirt = x.ndirt + sp;
+      }
+      x.ftodo = A.get<int>(std::max(x.nJ, 1));
+      x.ftodoP = A.get<int>(std::max(x.nP, 1));
+      x.nftodo = A.get<int>(2);
+    });
+    fp_on = true;
+  }
+
   void start_cache() {
     each([&](Slab &x) {
       x.nbx = (x.G.nx + BX - 1) / BX;
@@ -674,6 +747,15 @@ struct ShardedRun {
         throw Error{EXACTZ_ECUDA};
       }
     });
+    // the clean-path test for the list passes, as exactz_correct decides it
+    // (debug 0x80000: off; 0x200000: run whatever the dirty-tile count)
+    if (!(flags & (EXACTZ_NO_TRACK | EXACTZ_NO_C3 | 0x80000u | 0x100u | 0x400u))) {
+      static const double gate = [] {
+        const char *e = std::getenv("EXACTZ_FP_GATE");
+        return e ? std::atof(e) : 0.1;
+      }();
+      start_fpaths((flags & 0x200000u) ? 0.0 : gate);
+    }
   }
 
   // Gather every rank's keys (count in counter ci), sort identically on every
@@ -762,8 +844,48 @@ struct ShardedRun {
 
   template <bool SPLIT, bool FROM_REF>
   void events(Slab &x, const float *h, const int32_t *list, int n, int32_t *ext,
-              const Track *tr = nullptr) {
+              const Track *tr = nullptr, bool fpass = false) {
     if (n <= 0) return;
+    if (!FROM_REF && fpass && tr) {
+      // a list pass with the clean-path test (exactz_correct's launch_events):
+      // the saddles whose f-walk tiles are all clean take X_f; the rest (or
+      // what the stamp check left, with the cache on) are walked
+      const FPaths fp = SPLIT ? x.fpP : x.fpJ;
+      int *ftodo = SPLIT ? x.ftodoP : x.ftodo, *nft = x.nftodo + (SPLIT ? 1 : 0);
+      k_count_dirt<<<148, 256, 0, s>>>(fp.dirt, fp.nt, const_cast<unsigned long long *>(fp.ndirt));
+      CK(cudaMemsetAsync(nft, 0, sizeof(int), s));
+      const Slabs sb = slabs_of(SPLIT ? x.tup : x.tdn, x.cnt + C_CHANGED);
+      if (cache_on) {
+        const EvCache ec = SPLIT ? x.ecP : x.ecJ;
+        int *todo = SPLIT ? x.todoP : x.todo, *ntodo = x.ntodo + (SPLIT ? 1 : 0);
+        CK(cudaMemsetAsync(ntodo, 0, sizeof(int), s));
+        k_events_check<SPLIT, true><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+            list, n, ec, *tr, x.marks, x.G, todo, ntodo, x.cnt, nullptr, nullptr, x.remote);
+        k_fclean<SPLIT, true><<<148 * 4, 256, 0, s>>>(h, list, n, x.lm, x.ref, fp, ext, x.marks,
+                                                      x.G, ftodo, nft, x.cnt, todo, ntodo, ec,
+                                                      tr->round, fp.ndirt, fp.max_dirt, x.remote);
+        k_events_cached<SPLIT, true><<<148 * 16, 256, 0, s>>>(
+            h, list, ftodo, nft, x.slots, x.lm, ext, x.marks, x.G, ec, *tr, x.cnt, todo, ntodo, sb,
+            x.remote);
+        g_launches += 4;
+      } else {
+        k_fclean<SPLIT, true><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+            h, list, n, x.lm, x.ref, fp, ext, x.marks, x.G, ftodo, nft, x.cnt, nullptr, nullptr,
+            EvCache{}, 0, fp.ndirt, fp.max_dirt, x.remote);
+        // grids sized for every saddle (the list's length is on the device;
+        // a grid-stride grid made the walks slower)
+        if (n <= (1 << 19))
+          k_events16<SPLIT, true><<<(unsigned)((16 * (int64_t)n + 255) / 256), 256, 0, s>>>(
+              h, list, n, x.slots, x.lm, ext, x.marks, x.G, sb, x.remote, x.cnt, nullptr, ftodo,
+              nft);
+        else
+          k_events<SPLIT, false, true><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+              h, list, n, x.slots, x.lm, x.ref, ext, x.marks, x.G, sb, x.remote, x.cnt, ftodo, nft);
+        g_launches += 3;
+      }
+      CK(cudaGetLastError());
+      return;
+    }
     if (!FROM_REF && cache_on && tr) {
       // the stamp check re-emits the still valid results, the rest is walked
       // (k_events_cached, which caches what stays inside the slab)
@@ -862,10 +984,23 @@ struct ShardedRun {
     ++rnd;
     if (cache_on && rnd >= 65000) cache_on = false;  // 16-bit stamps (as exactz_correct)
     const bool tracked = act_on || cache_on;  // the stencils / edit keep tracking state
+    // the clean-path test in list passes (the list stencil flags the tiles
+    // holding a pointer that is not f's; an unlisted vertex has f's pointers)
+    const bool fpass = fp_on && act_on && ready && c3 && !reform;
+    if (fpass)
+      each([&](Slab &x) {
+        CK(cudaMemsetAsync(x.dirtD, 0, 2 * (((size_t)x.nt + 15) / 16 * 16) + 16, s));
+      });
     auto track = [&](Slab &x) {
       Track t{};
       t.round = rnd;
       t.tab_round = tab_round;
+      if (fpass) {
+        t.dirtD = x.dirtD;
+        t.dirtU = x.dirtU;
+        t.ntx = x.ntx;
+        t.nty = x.nty;
+      }
       if (act_on) {
         t.act_next = x.act[cur ^ 1];
         t.edited = x.edited;
@@ -1045,8 +1180,8 @@ struct ShardedRun {
     if (c3w)
       each([&](Slab &x) {
         const Track t = track(x);
-        events<false, false>(x, x.g, x.J, x.nJ, x.m1, &t);
-        events<true, false>(x, x.g, x.P, x.nP, x.M1, &t);
+        events<false, false>(x, x.g, x.J, x.nJ, x.m1, &t, fpass);
+        events<true, false>(x, x.g, x.P, x.nP, x.M1, &t, fpass);
       });
     CK(cudaGetLastError());
     // exchange B: the walks' targets owned by another rank (all-gathered)

@@ -73,13 +73,15 @@ def test_slabs_errors(exactz):
     assert E.status_of(E.exactz_correct_slabs, f.cuda(), bad.cuda(), xi, 2) == E.EBOUND
 
 
-@pytest.mark.parametrize("flags", [0x800000, 0x1000000, 0x2000000, 0x2000, 0x8000])
+@pytest.mark.parametrize("flags", [0x800000, 0x1000000, 0x2000000, 0x2000, 0x8000, 0x80000,
+                                   0x200000, 0x200])
 def test_slabs_engine_variants(exactz, flags):
     """Exchange and kernel variants of the per-rank engine, each bit-equal:
     boundary tables by sparse changes only (0x800000) or whole every pass
     (0x1000000); one-lane C3 walks (0x2000000); the float-compare stencils
     instead of the exact-key ones (0x2000); thread-staged planes instead of
-    TMA (0x8000)."""
+    TMA (0x8000); no clean-path test (0x80000) or the test in every list pass
+    (0x200000); no C3 cache (0x200)."""
     f, g, xi = S.make("C2", shape=(24, 20, 64))
     assert_same(*both(exactz, f, g, xi, 6, flags=flags))
 
