@@ -2594,6 +2594,33 @@ __global__ void k_gs_diff(const int32_t *__restrict__ own, int n, const uint32_t
   if (q >= 0) upd[q] = make_int2(k, (int)v);
 }
 
+// The same over the vertices a list pass evaluated (list[0 .. *nlist), local
+// ids): the f-saddles among them are the only owned entries that can change
+__global__ void k_gs_diff_list(const int32_t *__restrict__ list, const int *__restrict__ nlist,
+                               const uint32_t *__restrict__ ref, const int32_t *__restrict__ posS,
+                               const uint32_t *__restrict__ gS, uint32_t *prev, int2 *upd,
+                               unsigned long long *nupd) {
+  const int n = *nlist;
+  // block-uniform trip count (cta_slot synchronises the block)
+  for (int b = blockIdx.x * blockDim.x; b < n; b += gridDim.x * blockDim.x) {
+    const int j = b + threadIdx.x;
+    int k = 0;
+    uint32_t v = 0;
+    bool chg = false;
+    if (j < n) {
+      const int i = __ldg(&list[j]);
+      if (ref_saddle(__ldg(&ref[i]))) {
+        k = __ldg(&posS[i]);
+        v = gS[k];
+        chg = prev[k] != v;
+        if (chg) prev[k] = v;
+      }
+    }
+    const long long q = cta_slot(chg, nupd);
+    if (q >= 0) upd[q] = make_int2(k, (int)v);
+  }
+}
+
 // gathered (position, value bits) updates into the replicated gS (pos < 0: padding)
 __global__ void k_apply_gs(const int2 *__restrict__ upd, int n, uint32_t *gS) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;

@@ -629,9 +629,8 @@ struct ShardedRun {
     // O7 reference of f on the owned planes
     zero_counters();
     each([&](Slab &x) {
-      unsigned bx = std::min(8u, (unsigned)((nx + 127) / 128));
-      unsigned by = (unsigned)std::min<int64_t>((int64_t)x.nzl * ny, 148 * 16 / bx + 1);
-      k_reference<<<dim3(bx, by), 128, 0, s>>>(x.f, x.G, x.ref, x.keys, x.cpkeys, x.cnt);
+      // the z-marching tile kernel of exactz_correct over the owned planes
+      k_reference_tile<<<x.sgrid, 256, 0, s>>>(x.f, x.G, x.zc, x.ref, x.keys, x.cpkeys, x.cnt);
     });
     CK(cudaGetLastError());
     read_counters();
@@ -1083,7 +1082,13 @@ struct ShardedRun {
     const bool c3w = c3 && !reform;
     if (c2)
       each([&](Slab &x) {
-        if (x.nown)
+        // a late list pass (the cache on: the lists are short) re-evaluated
+        // only the listed vertices: only their saddles can have changed (an
+        // early list holds up to a quarter of the slab, more than its saddles)
+        if (act_on && ready && cache_on)
+          k_gs_diff_list<<<148 * 8, 256, 0, s>>>(x.list, x.nlist, x.ref, x.posS, x.gS, x.gSprev,
+                                                 x.upd, x.nrem + p + x.rank);
+        else if (x.nown)
           k_gs_diff<<<(x.nown + 255) / 256, 256, 0, s>>>(x.own, x.nown, x.gS, x.gSprev, x.upd,
                                                          x.nrem + p + x.rank);
       });
