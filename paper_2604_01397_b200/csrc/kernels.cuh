@@ -1327,18 +1327,21 @@ __global__ void k_scatter_pos(const int32_t *__restrict__ S, int n, int32_t *pos
 // FROM_REF: pointers of f (ref word bits 14-17 / 18-21); else of g (slot
 // bytes written by the stencil, low / high nibble).  Returns the local root,
 // or -(w + 1) for the first vertex w of the path outside the owned planes
-// (sharded slabs only; on a single GPU every path stays inside).
+// (sharded slabs only; on a single GPU every path stays inside).  A slab's
+// ghost-plane slot bytes hold kSelf in both nibbles (set at setup, never
+// written), so a g walk stops there by itself and is tested once at its end
+// instead of at every step; the ref words of f have no such planes.
 template <bool UP, bool FROM_REF, bool SLAB>
 __device__ __forceinline__ int walk(int u, const uint8_t *__restrict__ slots,
                                     const uint32_t *__restrict__ ref, const GridP &G) {
   const int A = G.nx * G.ny, lo = G.zb * A, hi = G.ze * A;
   int w = u;
   for (;;) {
-    if (SLAB && (w < lo || w >= hi)) return -(w + 1);
+    if (SLAB && FROM_REF && (w < lo || w >= hi)) return -(w + 1);
     int s;
     if (FROM_REF) s = (__ldg(&ref[w]) >> (UP ? 18 : 14)) & 15;
     else s = (__ldg(&slots[w]) >> (UP ? 4 : 0)) & 15;
-    if (s == kSelf) return w;
+    if (s == kSelf) return (SLAB && !FROM_REF && (w < lo || w >= hi)) ? -(w + 1) : w;
     const int b = slot_bits(s);
     const int d = (b & 1) + ((b >> 1) & 1) * G.nx + (b >> 2) * A;
     w += slot_sign(s) * d;
@@ -1361,13 +1364,17 @@ struct Slabs {
   int p;
   const int2 *table;  // 2 * p * A entries, or nullptr (single GPU)
   unsigned long long *err;  // set when a chain is longer than the table (never: acyclic)
+  int base = 0, extra = 0;  // the split: nz / p planes, the first nz % p ranks one more
 };
 
 __device__ __forceinline__ int2 table_entry(const Slabs &S, int xg, int A) {
   const int z = xg / A;
-  int r = 0;
-  while (r + 1 < S.p && S.start[r + 1] <= z) ++r;
-  const int side = (z == S.start[r]) ? 0 : 1;
+  // the rank owning plane z, from the split rule (exactz_slab_range) instead
+  // of a search through start[] (a chain of dependent loads per lookup)
+  const int big = S.extra * (S.base + 1);
+  const int r = z < big ? z / (S.base + 1) : S.extra + (z - big) / S.base;
+  const int zs = r * S.base + min(r, S.extra);
+  const int side = (z == zs) ? 0 : 1;
   return S.table[(size_t)(2 * r + side) * A + (xg - z * A)];
 }
 __device__ __forceinline__ int2 table_lookup(const Slabs &S, int xg, int A) {
@@ -1438,13 +1445,15 @@ __device__ __forceinline__ int walk_track(int u, int x, int y, int z,
   const int A = G.nx * G.ny;
   int w = u;
   for (;;) {
-    if (SLAB && (w < G.zb * A || w >= G.ze * A)) {
-      mask |= kExit;
-      return -(w + 1);
-    }
     brick_bit(x, y, z, bsx, bsy, bsz, mask);
     const int s = (__ldg(&slots[w]) >> (UP ? 4 : 0)) & 15;
-    if (s == kSelf) return w;
+    if (s == kSelf) {  // a root, or (slab) a ghost vertex: see walk()
+      if (SLAB && (w < G.zb * A || w >= G.ze * A)) {
+        mask |= kExit;
+        return -(w + 1);
+      }
+      return w;
+    }
     const int b = slot_bits(s), sg1 = slot_sign(s);
     x += sg1 * (b & 1);
     y += sg1 * ((b >> 1) & 1);
@@ -1650,8 +1659,11 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
       for (int j = 0; j < KW; ++j) {
         sv[j] = kSelf;
         if ((runm >> j) & 1u) {
-          if (!SLAB || (w[j] >= lo && w[j] < hi)) sv[j] = next_slot<SPLIT, FROM_REF>(w[j], slots, ref);
-          else sv[j] = -1;  // sharded: the exit into a neighbour's slab
+          // (slab, f walks: the exit into a neighbour's slab is tested per
+          // step; g walks stop at the ghost planes' kSelf slots, see walk())
+          if (!(SLAB && FROM_REF) || (w[j] >= lo && w[j] < hi))
+            sv[j] = next_slot<SPLIT, FROM_REF>(w[j], slots, ref);
+          else sv[j] = -1;
         }
       }
 #pragma unroll
@@ -1665,7 +1677,8 @@ __global__ void __launch_bounds__(256) k_events(const float *__restrict__ h,
         runm &= ~(1u << j);
         int lab;
         float val;
-        if (!SLAB || sv[j] >= 0) {
+        const bool exited = SLAB && (FROM_REF ? sv[j] < 0 : (w[j] < lo || w[j] >= hi));
+        if (!exited) {
           lab = w[j] + off;
           val = h[w[j]];
         } else {
@@ -1965,8 +1978,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
       for (int j = 0; j < 2; ++j) {
         sv[j] = kSelf;
         if ((runm >> j) & 1u) {
-          if (!SLAB || (w[j] >= lo && w[j] < hi)) sv[j] = (__ldg(&slots[w[j]]) >> (SPLIT ? 4 : 0)) & 15;
-          else sv[j] = -1;  // the exit into a neighbour's slab
+          sv[j] = (__ldg(&slots[w[j]]) >> (SPLIT ? 4 : 0)) & 15;  // (ghosts: kSelf, see walk())
         }
       }
 #pragma unroll
@@ -1984,7 +1996,7 @@ __global__ void __launch_bounds__(256) k_events_cached(const float *__restrict__
         runm &= ~(1u << j);
         int lab;
         float val;
-        if (!SLAB || sv[j] >= 0) {
+        if (!SLAB || (w[j] >= lo && w[j] < hi)) {
           lab = w[j] + off;
           val = h[w[j]];
         } else {  // completed from the boundary tables
@@ -2417,15 +2429,11 @@ __global__ void k_boundary_delta(const float *__restrict__ h, const uint8_t *__r
     if (walk) {
       unsigned long long mask = 0;
       int w = (side ? G.ze - 1 : G.zb) * A + xy, e;
-      for (;;) {  // walk(): the steepest path of g inside the slab
-        if (w < lo || w >= hi) {
-          e = -(w + 1);
-          break;
-        }
+      for (;;) {  // walk(): the steepest path of g inside the slab (ghosts: kSelf)
         if (CACHE) brick_bit(x, y, z, bsx, bsy, bsz, mask);
         const int sl = (__ldg(&slots[w]) >> sh) & 15;
         if (sl == kSelf) {
-          e = w;
+          e = (w < lo || w >= hi) ? -(w + 1) : w;
           break;
         }
         const int b = slot_bits(sl), sg1 = slot_sign(sl);

@@ -576,6 +576,10 @@ struct ShardedRun {
       CK(cudaMemcpyAsync(x.f + P, f_in[l], (size_t)x.nzl * P * 4, cudaMemcpyDefault, s));
       CK(cudaMemcpyAsync(x.g + P, g_in[l], (size_t)x.nzl * P * 4, cudaMemcpyDefault, s));
       CK(cudaMemsetAsync(x.c, 0, Vl, s));
+      // ghost-plane slots: kSelf in both nibbles, never written (a g walk
+      // stops at a ghost vertex by itself; walk())
+      CK(cudaMemsetAsync(x.slots, 0xEE, P, s));
+      CK(cudaMemsetAsync(x.slots + (size_t)(x.nzl + 1) * P, 0xEE, P, s));
       CK(cudaMemsetAsync(x.marks, 0, (size_t)G.nz * x.words_per_plane() * 4, s));
     }
     halo_planes(true);
@@ -815,7 +819,7 @@ struct ShardedRun {
   }
 
   Slabs slabs_of(const int2 *table, unsigned long long *err = nullptr) const {
-    return Slabs{d_start, p, table, err};
+    return Slabs{d_start, p, table, err, nz / p, nz % p};
   }
 
   // gather the boundary walk termini of every rank and resolve them
