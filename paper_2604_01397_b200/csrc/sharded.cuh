@@ -1084,7 +1084,10 @@ struct ShardedRun {
       CK(cudaGetLastError());
     }
     const bool c3w = c3 && !reform;
-    if (c2)
+    // the boundary tables serve walks that leave a slab, the exchanges other
+    // replicas and other owners: none of them with one rank
+    const bool tabs = c3w && p > 1;
+    if (c2 && p > 1)
       each([&](Slab &x) {
         // a late list pass (the cache on: the lists are short) re-evaluated
         // only the listed vertices: only their saddles can have changed (an
@@ -1099,7 +1102,7 @@ struct ShardedRun {
     // the g boundary tables (C3 walks that leave a slab): this rank's entries
     // recomputed; after the first pass only the changed ones travel
     const size_t A2 = (size_t)nx * ny;
-    if (c3w)
+    if (tabs)
       each([&](Slab &x) {
         CK(cudaMemsetAsync(x.nrem + 2 * p + x.rank, 0, 8, s));
         const unsigned nb = (unsigned)((4 * A2 + 255) / 256);
@@ -1115,7 +1118,7 @@ struct ShardedRun {
     // exchange A (before C2 and the walks): nrem[p, 2p) = each rank's changed
     // gS entries (counted by the stencils), nrem[2p, 3p) = its changed table
     // entries; one count exchange sizes both sparse all-gathers
-    if (c2 || c3w) {
+    if ((c2 || tabs) && p > 1) {
       std::vector<unsigned long long *> nb;
       each([&](Slab &x) { nb.push_back(x.nrem); });
       T.allreduce_sum_u64(nb, 3 * p);
@@ -1146,7 +1149,7 @@ struct ShardedRun {
       // 0x1000000: whole chunks every pass)
       const bool full = !tables_ready || (flags & 0x1000000u) ||
                         (2 * mt > A2 && !(flags & 0x800000u));
-      if (c3w && full) {
+      if (tabs && full) {
         // the first pass (or many changes): every rank's whole chunk, in place
         for (int up = 0; up < 2; ++up) {
           std::vector<const void *> snd;
@@ -1160,7 +1163,7 @@ struct ShardedRun {
         }
         tables_ready = true;
         tab_round = rnd;
-      } else if (c3w && mt) {
+      } else if (tabs && mt) {
         tab_round = rnd;  // (cached walks that used the tables are stale)
         if (mt * p > x_alltupd_cap()) grow_alltupd(mt * p);
         std::vector<const void *> snd;
@@ -1194,7 +1197,7 @@ struct ShardedRun {
       });
     CK(cudaGetLastError());
     // exchange B: the walks' targets owned by another rank (all-gathered)
-    if (c3w) {
+    if (c3w && p > 1) {
       std::vector<unsigned long long *> nb;
       each([&](Slab &x) {
         CK(cudaMemsetAsync(x.nrem, 0, p * 8, s));
