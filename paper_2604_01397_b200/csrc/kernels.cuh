@@ -2629,6 +2629,57 @@ __global__ void k_gs_diff_list(const int32_t *__restrict__ list, const int *__re
   }
 }
 
+// R4 partner values (static routing): the pair (S[k], S[k+1]) is checked by
+// the owner of S[k], which needs g at S[k+1].  Every rank computes, from the
+// replicated S, the positions it sends (its own j whose predecessor S[j-1] is
+// another rank's: key = that rank) and receives (S[k+1] of its own k owned by
+// another rank: key = that rank); sorted by key, both sides list a pair's
+// positions in ascending order, so the values need no positions on the wire.
+__device__ __forceinline__ int owner_rank(int v, int A, int base, int extra) {
+  const int z = v / A, big = extra * (base + 1);
+  return z < big ? z / (base + 1) : extra + (z - big) / base;
+}
+__global__ void k_r4_route(const int32_t *__restrict__ own, int nown,
+                           const int32_t *__restrict__ S, int nS, int A, int base, int extra,
+                           int me, int p, int32_t *skey, int32_t *spos, int32_t *rkey,
+                           int32_t *rpos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nown) return;
+  const int k = __ldg(&own[i]);
+  int d = p, r = p;  // p: nothing to send / receive (sorted last)
+  if (k >= 1) {
+    const int o = owner_rank(__ldg(&S[k - 1]), A, base, extra);
+    if (o != me) d = o;
+  }
+  if (k + 1 < nS) {
+    const int o = owner_rank(__ldg(&S[k + 1]), A, base, extra);
+    if (o != me) r = o;
+  }
+  skey[i] = d;
+  spos[i] = k;
+  rkey[i] = r;
+  rpos[i] = k + 1;
+}
+// first index of each key in a sorted key array (start[0 .. p], start[p] = n
+// of the keys < p); start[] preset to n by the caller
+__global__ void k_key_starts(const int32_t *__restrict__ key, int n, int p, int *start) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int k = key[i];
+  if (i == 0 || key[i - 1] != k)
+    for (int q = i == 0 ? 0 : key[i - 1] + 1; q <= k && q <= p; ++q) start[q] = i;
+}
+__global__ void k_pack_u32(const int32_t *__restrict__ pos, int n, const uint32_t *__restrict__ v,
+                           uint32_t *out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = v[pos[i]];
+}
+__global__ void k_unpack_u32(const int32_t *__restrict__ pos, int n, const uint32_t *__restrict__ in,
+                             uint32_t *v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[pos[i]] = in[i];
+}
+
 // gathered (position, value bits) updates into the replicated gS (pos < 0: padding)
 __global__ void k_apply_gs(const int2 *__restrict__ upd, int n, uint32_t *gS) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;

@@ -63,6 +63,15 @@ struct Transport {
                          size_t bytes) = 0;
   virtual void allreduce_sum_u64(const std::vector<unsigned long long *> &buf, size_t n) = 0;
   virtual void allreduce_max_u32(const std::vector<uint32_t *> &buf, size_t n) = 0;
+  // All-to-all of 4-byte words with per-peer counts and offsets (words),
+  // one entry per local rank: send[soff[q] ..+ scnt[q]) -> peer q's recv at
+  // its roff[me].  The plans are static for a run (the loopback caches them).
+  struct Ata {
+    const uint32_t *send = nullptr;
+    uint32_t *recv = nullptr;
+    std::vector<size_t> soff, scnt, roff, rcnt;
+  };
+  virtual void alltoallv_u32(const std::vector<Ata> &a) = 0;
 };
 
 __global__ void k_sum_u64(unsigned long long *acc, const unsigned long long *src, int n) {
@@ -122,10 +131,25 @@ __global__ void k_loop_reduce(LoopMPtrs buf, int p, size_t n) {
   for (int l = 0; l < p; ++l) reinterpret_cast<T *>(buf.a[l])[k] = v;
 }
 
+struct CopySeg {
+  const char *src;
+  char *dst;
+  size_t bytes;
+};
+// segment blockIdx.y of a descriptor list
+__global__ void k_loop_segs(const CopySeg *__restrict__ seg) {
+  const CopySeg g = seg[blockIdx.y];
+  seg_copy(g.dst, g.src, g.bytes);
+}
+
 struct LoopTransport : Transport {
   int p;
   cudaStream_t s;
   Arena &arena;
+  CopySeg *ata_seg = nullptr;  // the cached all-to-all plan (device), its key
+  const void *ata_key = nullptr;
+  int ata_n = 0;
+  size_t ata_max = 0;
   LoopTransport(int p_, cudaStream_t s_, Arena &a) : p(p_), s(s_), arena(a) {}
   int nranks() const override { return p; }
   int nlocal() const override { return p; }
@@ -187,6 +211,31 @@ struct LoopTransport : Transport {
     CK(cudaGetLastError());
     for (int l = 1; l < p; ++l) CK(cudaMemcpyAsync(buf[l], buf[0], n * 8, cudaMemcpyDefault, s));
   }
+  void alltoallv_u32(const std::vector<Ata> &a) override {
+    if (ata_key != (const void *)a[0].send) {  // build the segment list once per plan
+      std::vector<CopySeg> segs;
+      size_t mx = 0;
+      for (int r = 0; r < p; ++r)
+        for (int q = 0; q < p; ++q)
+          if (q != r && a[r].scnt[q]) {
+            segs.push_back(CopySeg{(const char *)(a[r].send + a[r].soff[q]),
+                                   (char *)(a[q].recv + a[q].roff[r]), a[r].scnt[q] * 4});
+            mx = std::max(mx, a[r].scnt[q] * 4);
+          }
+      ata_n = (int)segs.size();
+      ata_max = mx;
+      if (ata_n) {
+        ata_seg = arena.get<CopySeg>(segs.size());
+        CK(cudaMemcpyAsync(ata_seg, segs.data(), segs.size() * sizeof(CopySeg),
+                           cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // (segs is a host temporary)
+      }
+      ata_key = a[0].send;
+    }
+    if (!ata_n) return;
+    k_loop_segs<<<dim3(seg_blocks(ata_max), ata_n), 256, 0, s>>>(ata_seg);
+    CK(cudaGetLastError());
+  }
   void allreduce_max_u32(const std::vector<uint32_t *> &buf, size_t n) override {
     if (p < 2 || !n) return;
     if (p <= kLoopMax) {
@@ -242,6 +291,16 @@ struct NcclTransport : Transport {
   void allreduce_max_u32(const std::vector<uint32_t *> &buf, size_t n) override {
     if (n) NK(ncclAllReduce(buf[0], buf[0], n, ncclUint32, ncclMax, c->nccl, s));
   }
+  void alltoallv_u32(const std::vector<Ata> &a) override {
+    const int me = c->rank, p = c->nranks;
+    NK(ncclGroupStart());
+    for (int q = 0; q < p; ++q) {
+      if (q == me) continue;
+      if (a[0].scnt[q]) NK(ncclSend(a[0].send + a[0].soff[q], a[0].scnt[q], ncclUint32, q, c->nccl, s));
+      if (a[0].rcnt[q]) NK(ncclRecv(a[0].recv + a[0].roff[q], a[0].rcnt[q], ncclUint32, q, c->nccl, s));
+    }
+    NK(ncclGroupEnd());
+  }
 };
 
 // Planes of rank r in an nz-plane field split over p ranks: the first nz % p
@@ -285,6 +344,12 @@ struct Slab {
   // saddles (local index), this round's changed entries, all ranks' lists
   int32_t *posS = nullptr;
   uint32_t *gSprev = nullptr;  // the owned entries as last listed (k_gs_diff)
+  // R4 partner values by static routing (k_r4_route): positions sent /
+  // received (grouped by peer), their buffers, the per-peer plan
+  int32_t *r4s = nullptr, *r4r = nullptr;
+  uint32_t *r4sbuf = nullptr, *r4rbuf = nullptr;
+  int r4ns = 0, r4nr = 0;
+  std::vector<size_t> r4soff, r4scnt, r4roff, r4rcnt;
   int2 *upd = nullptr, *allupd = nullptr;
   unsigned long long *cnt = nullptr, *hcnt = nullptr;  // device counters / host mirror
   unsigned long long *nrem = nullptr;                    // per-rank remote counts (p)
@@ -729,6 +794,7 @@ struct ShardedRun {
         x.gSprev = A.get<uint32_t>(nS);
         CK(cudaMemcpyAsync(x.gSprev, x.gS, (size_t)nS * 4, cudaMemcpyDeviceToDevice, s));
       });
+      if (p > 1) r4_routes();
     }
     if (reform) {
       gather_sorted(C_NCP, [](Slab &x) { return x.cpkeys; },
@@ -759,6 +825,74 @@ struct ShardedRun {
       }();
       start_fpaths((flags & 0x200000u) ? 0.0 : gate);
     }
+  }
+
+  // The static R4 routing (see k_r4_route): per slab the positions it sends
+  // and receives, grouped by peer, in ascending order within a peer.
+  void r4_routes() {
+    const int A2 = nx * ny, base = nz / p, extra = nz % p;
+    int bits = 1;
+    while ((1 << bits) <= p) ++bits;
+    each([&](Slab &x) {
+      x.r4soff.assign(p, 0);
+      x.r4scnt.assign(p, 0);
+      x.r4roff.assign(p, 0);
+      x.r4rcnt.assign(p, 0);
+      const int n = x.nown;
+      x.r4sbuf = A.get<uint32_t>(std::max(n, 1));
+      x.r4rbuf = A.get<uint32_t>(std::max(n, 1));
+      if (!n) return;
+      int32_t *k0 = A.get<int32_t>(n), *p0 = A.get<int32_t>(n), *k1 = A.get<int32_t>(n),
+              *p1 = A.get<int32_t>(n);
+      int32_t *sk = A.get<int32_t>(n), *rk = A.get<int32_t>(n);
+      x.r4s = A.get<int32_t>(n);
+      x.r4r = A.get<int32_t>(n);
+      k_r4_route<<<(n + 255) / 256, 256, 0, s>>>(x.own, n, x.S, nS, A2, base, extra, x.rank, p, k0,
+                                                 p0, k1, p1);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, sk, p0, x.r4s, n, 0, bits, s));
+      void *tmp = A.get<uint8_t>(tb);
+      CK(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, sk, p0, x.r4s, n, 0, bits, s));
+      CK(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, rk, p1, x.r4r, n, 0, bits, s));
+      int *st = A.get<int>(2 * (p + 1));
+      std::vector<int> init(2 * (p + 1), n);
+      CK(cudaMemcpyAsync(st, init.data(), init.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      k_key_starts<<<(n + 255) / 256, 256, 0, s>>>(sk, n, p, st);
+      k_key_starts<<<(n + 255) / 256, 256, 0, s>>>(rk, n, p, st + p + 1);
+      CK(cudaGetLastError());
+      std::vector<int> h(2 * (p + 1));
+      CK(cudaMemcpyAsync(h.data(), st, h.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+      sync();
+      for (int q = 0; q < p; ++q) {
+        x.r4soff[q] = (size_t)h[q];
+        x.r4scnt[q] = (size_t)(h[q + 1] - h[q]);
+        x.r4roff[q] = (size_t)h[p + 1 + q];
+        x.r4rcnt[q] = (size_t)(h[p + 2 + q] - h[p + 1 + q]);
+      }
+      x.r4ns = h[p];
+      x.r4nr = h[2 * p + 1];
+    });
+  }
+  // The partner values of this pass's R4 pairs, by the static routing
+  void r4_exchange() {
+    std::vector<Transport::Ata> plan;
+    each([&](Slab &x) {
+      if (x.r4ns) k_pack_u32<<<(x.r4ns + 255) / 256, 256, 0, s>>>(x.r4s, x.r4ns, x.gS, x.r4sbuf);
+      Transport::Ata a;
+      a.send = x.r4sbuf;
+      a.recv = x.r4rbuf;
+      a.soff = x.r4soff;
+      a.scnt = x.r4scnt;
+      a.roff = x.r4roff;
+      a.rcnt = x.r4rcnt;
+      plan.push_back(a);
+    });
+    CK(cudaGetLastError());
+    T.alltoallv_u32(plan);
+    each([&](Slab &x) {
+      if (x.r4nr) k_unpack_u32<<<(x.r4nr + 255) / 256, 256, 0, s>>>(x.r4r, x.r4nr, x.r4rbuf, x.gS);
+    });
+    CK(cudaGetLastError());
   }
 
   // Gather every rank's keys (count in counter ci), sort identically on every
@@ -1130,7 +1264,16 @@ struct ShardedRun {
         mu = std::max(mu, counts[p + r]);
         mt = std::max(mt, counts[2 * p + r]);
       }
-      if (c2 && mu) {
+      // R4 needs only the partners' values: when the changes are many (the
+      // dense passes), the static routing moves ~nS / p words per rank
+      // instead of p x mu (position, value) pairs (the same decision on every
+      // rank; debug 0x10000000: never, 0x20000000: always)
+      const bool r4static = c2 && !(flags & 0x10000000u) &&
+                            ((flags & 0x20000000u) ||
+                             (unsigned long long)mu * p * p > (unsigned long long)nS);
+      if (r4static) {
+        r4_exchange();
+      } else if (c2 && mu) {
         std::vector<const void *> snd;
         std::vector<void *> rcv;
         each([&](Slab &x) {  // pad to mu with position -1
