@@ -391,6 +391,10 @@ struct ShardedRun {
   uint32_t flags;
   bool act_on = false, ready = false;  // vertex activity started / act[cur] valid
   bool cache_on = false;               // the C3 cache started
+  // stars of this pass's edits: pulled next pass (edited bitmap, dilated by
+  // k_act_list) when many, pushed into act_next by the edit when few, as
+  // exactz_correct decides (set by the caller from the global V_t)
+  bool pull = true, edited_valid = false;
   bool fp_on = false;                  // the clean-path test is set up (list passes use it)
   int rnd = 0;                         // pass number (16-bit stamps of the cache)
   int tab_round = 0;                   // last pass in which a g boundary-table entry changed
@@ -1140,7 +1144,7 @@ struct ShardedRun {
       }
       if (act_on) {
         t.act_next = x.act[cur ^ 1];
-        t.edited = x.edited;
+        t.edited = pull ? x.edited : nullptr;
       }
       if (cache_on) {
         t.bval = x.bval;
@@ -1162,10 +1166,11 @@ struct ShardedRun {
     if (c2) each([&](Slab &x) { CK(cudaMemsetAsync(x.nrem + p, 0, p * 8, s)); });
     if (c3 && !reform) each([&](Slab &x) { CK(cudaMemsetAsync(x.nrem + 2 * p, 0, p * 8, s)); });
     if (act_on && ready) {  // list-based pass: fired | stars of the last pass's edits
-      halo_edited();
+      if (edited_valid) halo_edited();
       each([&](Slab &x) {
         CK(cudaMemsetAsync(x.nlist, 0, sizeof(int), s));
-        k_act_list<<<148 * 16, 256, 0, s>>>(x.act[cur], x.edited, x.G, x.list, x.nlist);
+        k_act_list<<<148 * 16, 256, 0, s>>>(x.act[cur], edited_valid ? x.edited : nullptr, x.G,
+                                            x.list, x.nlist);
         if (x.keyed)
           k_stencil_list_key<<<148 * 16, 256, 0, s>>>(x.g, x.ref, x.marks, x.slots, x.lm, x.list,
                                                        x.nlist, x.G, track(x), x.cnt);
@@ -1399,7 +1404,8 @@ struct ShardedRun {
     }
     each([&](Slab &x) {
       if (tracked) {
-        if (act_on) CK(cudaMemsetAsync(x.edited, 0, (size_t)x.G.nz * x.words_per_plane() * 4, s));
+        if (act_on && pull)
+          CK(cudaMemsetAsync(x.edited, 0, (size_t)x.G.nz * x.words_per_plane() * 4, s));
         k_count_edit<true><<<148 * 8, 256, 0, s>>>(x.g, x.c, x.marks, x.f, x.G, xi, delta, N,
                                                     do_edit ? 1 : 0, track(x), x.cnt);
       } else {
@@ -1408,10 +1414,37 @@ struct ShardedRun {
       }
     });
     CK(cudaGetLastError());
+    if (act_on && !pull && p > 1) {
+      // pushed stars that fall in a ghost plane belong to the neighbour's
+      // boundary plane (as the marks above)
+      std::vector<const void *> lo, hi;
+      std::vector<void *> rlo, rhi;
+      each([&](Slab &x) {
+        const size_t W = x.words_per_plane();
+        uint32_t *an = x.act[cur ^ 1];
+        CK(cudaMemsetAsync(x.ghost_lo, 0, W * 4, s));
+        CK(cudaMemsetAsync(x.ghost_hi, 0, W * 4, s));
+        lo.push_back(an);
+        hi.push_back(an + (x.nzl + 1) * W);
+        rlo.push_back(x.ghost_lo);
+        rhi.push_back(x.ghost_hi);
+      });
+      T.halo(lo, hi, rlo, rhi, sl[0].words_per_plane() * 4);
+      each([&](Slab &x) {
+        const int W = (int)x.words_per_plane();
+        uint32_t *an = x.act[cur ^ 1];
+        k_or_words<<<(W + 255) / 256, 256, 0, s>>>(an + 1 * W, x.ghost_lo, W);
+        k_or_words<<<(W + 255) / 256, 256, 0, s>>>(an + x.nzl * W, x.ghost_hi, W);
+        CK(cudaMemsetAsync(an, 0, W * 4, s));
+        CK(cudaMemsetAsync(an + (x.nzl + 1) * W, 0, W * 4, s));
+      });
+      CK(cudaGetLastError());
+    }
     if (act_on) {  // act_next (| stars of `edited`) is the next pass's set
       cur ^= 1;
       ready = true;
     }
+    edited_valid = act_on && pull;
     allreduce_counters();
     read_counters();
     if (c3 && !reform && sl[0].hcnt[C_CHANGED]) {  // the boundary tables' verification round
@@ -1480,6 +1513,8 @@ static exactz_status sharded_impl(Transport &T, std::vector<const float *> f_in,
           rows < 65000 && prev_vt * cache_div <= nbg)
         R.start_cache();
     }
+    // (debug 0x40000000: always pull, the r02 behaviour before)
+    R.pull = (flags & 0x40000000u) || prev_vt * 256 > (unsigned long long)V;
     unsigned long long o[8];
     R.round(may_edit, o);
     prev_vt = o[C_VT];

@@ -74,7 +74,7 @@ def test_slabs_errors(exactz):
 
 
 @pytest.mark.parametrize("flags", [0x800000, 0x1000000, 0x2000000, 0x2000, 0x8000, 0x80000,
-                                   0x200000, 0x200, 0x10000000, 0x20000000])
+                                   0x200000, 0x200, 0x10000000, 0x20000000, 0x40000000])
 def test_slabs_engine_variants(exactz, flags):
     """Exchange and kernel variants of the per-rank engine, each bit-equal:
     boundary tables by sparse changes only (0x800000) or whole every pass
@@ -83,7 +83,7 @@ def test_slabs_engine_variants(exactz, flags):
     TMA (0x8000); no clean-path test (0x80000) or the test in every list pass
     (0x200000); no C3 cache (0x200); R4 partner values by the sparse
     all-gather only (0x10000000) or by the static routing in every pass
-    (0x20000000)."""
+    (0x20000000); the stars of the edits always pulled (0x40000000)."""
     f, g, xi = S.make("C2", shape=(24, 20, 64))
     assert_same(*both(exactz, f, g, xi, 6, flags=flags))
 
