@@ -730,7 +730,16 @@ struct ShardedRun {
     each([&](Slab &x) {
       uint64_t *pad = A.get<uint64_t>(slot);
       CK(cudaMemsetAsync(pad, 0xff, slot * 8, s));  // UINT64_MAX sorts last
-      CK(cudaMemcpyAsync(pad, x.keys, counts[x.rank] * 8, cudaMemcpyDeviceToDevice, s));
+      // each rank sorts its own keys; the gathered sorted runs are merged
+      // below (a replicated radix sort of all nS keys cost every rank ~2 ms
+      // at C5 / 8)
+      const int nk = (int)counts[x.rank];
+      if (nk) {
+        size_t tb0 = 0;
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, tb0, x.keys, pad, nk, 0, 64, s));
+        void *tmp0 = A.get<uint8_t>(tb0);
+        CK(cub::DeviceRadixSort::SortKeys(tmp0, tb0, x.keys, pad, nk, 0, 64, s));
+      }
       x.allkeys = A.get<uint64_t>(slot * p);
       x.sorted = A.get<uint64_t>(slot * p);
       ks.push_back(pad);
@@ -739,12 +748,37 @@ struct ShardedRun {
     T.allgather(ks, ka, slot * 8);
     each([&](Slab &x) {
       x.S = A.get<int32_t>(std::max(nS, 1));
-      size_t tb = 0;
-      CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, x.allkeys, x.sorted, (int)(slot * p), 0, 64,
-                                        s));
-      void *tmp = A.get<uint8_t>(tb);
-      CK(cub::DeviceRadixSort::SortKeys(tmp, tb, x.allkeys, x.sorted, (int)(slot * p), 0, 64, s));
-      if (nS) k_keys_to_ids<<<(nS + 255) / 256, 256, 0, s>>>(x.sorted, x.S, nS);
+      // pairwise merges of the p sorted runs (padding sorts last in each run
+      // and stays after the nS keys)
+      uint64_t *a = x.allkeys, *b = x.sorted;
+      const size_t total = slot * p;
+      size_t tbm = 0;
+      if (p > 1) {
+        const int h = (int)std::min<size_t>(total / 2, (size_t)INT32_MAX);
+        CK(cub::DeviceMerge::MergeKeys(nullptr, tbm, a, h, a + h, h, b, ::cuda::std::less<>{}, s));
+      }
+      void *tmpm = tbm ? A.get<uint8_t>(tbm) : nullptr;
+      for (size_t L = slot; L < total; L *= 2) {
+        for (size_t st = 0; st < total; st += 2 * L) {
+          const size_t n1 = std::min(L, total - st), n2 = st + L < total ? std::min(L, total - st - L) : 0;
+          if (n2) {
+            size_t need = 0;
+            CK(cub::DeviceMerge::MergeKeys(nullptr, need, a + st, (int)n1, a + st + L, (int)n2, b + st,
+                                           ::cuda::std::less<>{}, s));
+            if (need > tbm) {
+              tbm = need;
+              tmpm = A.get<uint8_t>(tbm);
+            }
+            CK(cub::DeviceMerge::MergeKeys(tmpm, need, a + st, (int)n1, a + st + L, (int)n2, b + st,
+                                           ::cuda::std::less<>{}, s));
+          } else {
+            CK(cudaMemcpyAsync(b + st, a + st, n1 * 8, cudaMemcpyDeviceToDevice, s));
+          }
+        }
+        std::swap(a, b);
+      }
+      x.sorted = a;  // (the merged keys)
+      if (nS) k_keys_to_ids<<<(nS + 255) / 256, 256, 0, s>>>(a, x.S, nS);
       x.gS = A.get<uint32_t>(std::max(nS, 1));
       // (a walk target per join and per split saddle the slab owns)
       x.remote = A.get<int32_t>(2 * (size_t)std::max(nS, 1));
